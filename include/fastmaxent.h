@@ -1,0 +1,134 @@
+/*
+ * fastmaxent.h -- C-ABI of the B200 (sm_100a) sampler for the MaxEnt configuration models of
+ * arXiv 2509.13230, "Fast unbiased sampling of networks with given expected degrees and
+ * strengths" (PAPER.md, cited P:L<n>).
+ *
+ * The library samples simple undirected graphs in which every unordered pair {i, j} is an
+ * edge independently with probability
+ *     UBCM  p_ij = x_i x_j / (1 + x_i x_j)                       (x = e^-alpha)
+ *     ECM   p_ij = z / (1 - t + z),  z = x_i y_i x_j y_j, t = y_i y_j   (Eq. 4, y = e^-beta)
+ * with ECM edge weights w >= 1, P(w) = t^{w-1} (1 - t)            (Eq. 5),
+ * by the Miller-Hagberg-style sorted geometric-skip rejection sampler of P:L127-136 (UBCM)
+ * and Algorithm 1, P:L144-166 (ECM), with the readings listed in DESIGN.md section 3.
+ *
+ * Conventions for every entry point:
+ *  - Returns an fm_status; never aborts.  On error nothing is allocated, *out is zeroed, and
+ *    fm_last_error() returns a thread-local message.
+ *  - All work is ordered on the caller's CUDA stream `cuda_stream` (cudaStream_t; NULL = the
+ *    legacy default stream) on the current device.
+ *  - Input pointers may be HOST or DEVICE memory (detected with cudaPointerGetAttributes); they
+ *    are borrowed for the duration of the call only.
+ *  - Objects returned through *out are library-owned; release them with fm_free().
+ *  - Results are pure functions of (x, y, seg_target, seed, sample index): sample k is
+ *    bit-identical whether produced alone or inside a batch (R1).
+ */
+#ifndef FASTMAXENT_H
+#define FASTMAXENT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FM_ABI_VERSION 1
+
+typedef enum {
+    FM_OK = 0,
+    FM_ERR_INVALID = -1, /* bad argument: N < 2 or > 2^31-1, NULL pointer, x not finite or < 0,
+                            y not in [0,1), kappa_max^2 overflow, seg_target out of range,
+                            sample range beyond 2^32 */
+    FM_ERR_NOMEM = -2,   /* device or host allocation failed */
+    FM_ERR_CUDA = -3,    /* CUDA runtime error (no device, launch failure, ...) */
+    FM_ERR_BOUND = -4,   /* contract violation p > q (1 + 2^-50) detected (debug checks) */
+    FM_ERR_STATE = -5    /* wrong object / model mismatch / internal invariant violated */
+} fm_status;
+
+typedef enum { FM_UBCM = 0, FM_ECM = 1 } fm_model;
+
+enum {
+    FM_FLAG_WEIGHT_SATURATED = 1u, /* an ECM weight exceeded INT32_MAX and was clamped (R8) */
+    FM_FLAG_SCRATCH_RERUN = 2u     /* some chunks overflowed their scratch and were re-run (same result) */
+};
+
+/* Opaque, immutable sampling plan: the sorted order (P:L133 step (i); Alg. 1 line 3), the
+ * beta_min suffix maximum, and the segment table of the planner.
+ * Device-resident; safe to use concurrently from several streams once created. */
+typedef struct fm_plan fm_plan;
+
+/* Sampled edge lists: n_samples graphs, concatenated. */
+typedef struct {
+    int64_t n_samples;
+    int64_t n_edges;   /* total over all samples */
+    int64_t *offsets;  /* HOST int64[n_samples + 1]: sample s = edges[offsets[s] .. offsets[s+1]) */
+    int32_t *edges;    /* DEVICE int32[2 * n_edges]: pairs (src, dst), src < dst, original ids
+                          ("Edge list E"; no self loops, no duplicates)                    */
+    int32_t *weights;  /* DEVICE int32[n_edges] (ECM, w >= 1), NULL for UBCM                         */
+    int64_t draws;     /* counters summed over samples: geometric draws incl. terminal ones     */
+    int64_t landed;    /* proposals (candidates reached, p/q tests)                              */
+    int64_t accepted;  /* == n_edges                                                             */
+    int64_t segments;  /* plan segments x n_samples                                             */
+    int64_t chunks;    /* warp chunks x n_samples                                               */
+    uint32_t flags;    /* FM_FLAG_*                                                              */
+    void *_owner;      /* internal                                                               */
+} fm_edges;
+
+typedef struct {
+    int32_t model;
+    int64_t n;
+    int64_t seg_target;
+    int32_t F;            /* fixed-point exponent of the planner (DESIGN.md 3.4 step 1) */
+    int64_t n_segments;
+    int64_t n_chunks;
+    int64_t est_draws;    /* planner estimate of draws per sample (sum of segment work) */
+} fm_plan_info;
+
+/* a1-a4.  Validate the fitness vectors, sort the nodes by descending kappa (x for UBCM,
+ * x*y for ECM; ties by ascending id), build the beta_min suffix maximum (ECM) and the segment
+ * plan.  x: float64[n] (x_i = e^{-alpha_i} >= 0), y: float64[n] (ECM: y_i = e^{-beta_i} in
+ * [0,1); must be NULL for UBCM).  seg_target S: expected draws per hub-row segment, 0 = 256,
+ * otherwise 8 <= S <= 2^40 (S changes results; R15).  Synchronises the stream once. */
+fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double *y,
+                       int64_t seg_target, void *cuda_stream, fm_plan **plan_out);
+
+/* a5-a6.  Draw n_samples graphs (sample indices first_sample .. first_sample+n_samples-1,
+ * first_sample + n_samples <= 2^32) from the UBCM with Philox key `seed`.
+ * Fills *out (device edges, host offsets).  Synchronises the stream once (to size the output).
+ * FM_ERR_STATE if the plan is an ECM plan.  n_samples == 0 returns an empty result. */
+fm_status fm_sample_ubcm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                         void *cuda_stream, fm_edges *out);
+
+/* As fm_sample_ubcm for the weighted ECM (Algorithm 1; Eq. 3-6): also fills
+ * out->weights.  FM_ERR_STATE if the plan is a UBCM plan. */
+fm_status fm_sample_ecm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                        void *cuda_stream, fm_edges *out);
+
+/* Copy a result to caller-owned HOST buffers: edges_host int32[2*n_edges], weights_host
+ * int32[n_edges] (may be NULL).  Stream-ordered; synchronises the stream. */
+fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host,
+                           void *cuda_stream);
+
+/* Plan metadata (host struct, caller-owned). */
+fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info);
+
+/* Inspection: copy plan arrays to caller-owned HOST buffers (any may be NULL):
+ * perm int32[n] (rank -> id), kappa_s float64[n], y_s float64[n] (ECM), ymax float64[n+1] (ECM),
+ * seg int32[4*n_segments] as (u, a, b, sigma), seg_h0/seg_q0/seg_omT float64[n_segments].
+ * Synchronises the current device. */
+fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax,
+                         int32_t *seg, double *seg_h0, double *seg_q0, double *seg_omT);
+
+/* Release an fm_plan* or the buffers of an fm_edges* (the struct itself is caller-owned and
+ * is zeroed).  Objects are tagged; NULL is a no-op. */
+void fm_free(void *obj);
+
+/* Thread-local message describing the last non-OK status. */
+const char *fm_last_error(void);
+
+/* FM_ABI_VERSION of the loaded library. */
+int32_t fm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTMAXENT_H */

@@ -1,0 +1,521 @@
+// fm_capi.cu -- the C-ABI (include/fastmaxent.h): validation, stream-ordered memory, launch
+// orchestration of the a1-a6 kernels, status codes.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "fm_internal.cuh"
+#include "fm_plan_kernels.cuh"
+
+using namespace fm;
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_mu;
+std::set<const void *> g_plans;
+std::set<const void *> g_owners;
+
+fm_status fail(fm_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+fm_status cuda_fail(cudaError_t e, const char *what)
+{
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(FM_ERR_NOMEM, "%s: %s", what, cudaGetErrorString(e));
+    }
+    return fail(FM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// Device allocations of one call; everything not released is freed (stream-ordered) on exit.
+struct Allocs {
+    cudaStream_t st;
+    std::vector<void *> ptrs;
+    explicit Allocs(cudaStream_t s) : st(s) {}
+    ~Allocs()
+    {
+        for (void *p : ptrs)
+            if (p) cudaFreeAsync(p, st);
+    }
+    template <typename T>
+    cudaError_t get(T **p, size_t count)
+    {
+        *p = nullptr;
+        if (count == 0) count = 1;
+        cudaError_t e = cudaMallocAsync((void **)p, count * sizeof(T), st);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+    void release(void *p)
+    {
+        for (auto &q : ptrs)
+            if (q == p) q = nullptr;
+    }
+};
+
+void configure_pool_once(int dev)
+{
+    static std::once_flag once;
+    std::call_once(once, [dev]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+bool is_device_ptr(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int ceil_log2(int64_t n)
+{
+    int L = 0;
+    while ((int64_t(1) << L) < n) L++;
+    return L;
+}
+
+int64_t env_i64(const char *name, int64_t dflt)
+{
+    const char *v = getenv(name);
+    if (!v || !*v) return dflt;
+    return strtoll(v, nullptr, 10);
+}
+
+unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+void plan_release(Plan *p)
+{
+    if (!p) return;
+    cudaFree(p->perm);
+    cudaFree(p->kappa_s);
+    cudaFree(p->y_s);
+    cudaFree(p->ymax);
+    cudaFree(p->seg);
+    cudaFree(p->seg_h0);
+    cudaFree(p->seg_q0);
+    cudaFree(p->seg_omT);
+    cudaFree(p->chunk_seg);
+    p->magic = 0;
+    delete p;
+}
+
+bool plan_live(const void *p)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    return g_plans.count(p) != 0;
+}
+
+}  // namespace
+
+#define CK(expr, what)                                            \
+    do {                                                          \
+        cudaError_t e_ = (expr);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what);        \
+    } while (0)
+
+extern "C" {
+
+const char *fm_last_error(void) { return g_err.c_str(); }
+int32_t fm_abi_version(void) { return FM_ABI_VERSION; }
+
+fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double *y, int64_t seg_target,
+                       void *cuda_stream, fm_plan **plan_out)
+{
+    if (!plan_out) return fail(FM_ERR_INVALID, "plan_out is NULL");
+    *plan_out = nullptr;
+    if (model != FM_UBCM && model != FM_ECM) return fail(FM_ERR_INVALID, "unknown model %d", (int)model);
+    if (n < 2 || n > INT32_MAX) return fail(FM_ERR_INVALID, "n = %lld outside [2, 2^31-1]", (long long)n);
+    if (!x) return fail(FM_ERR_INVALID, "x is NULL");
+    if (model == FM_ECM && !y) return fail(FM_ERR_INVALID, "ECM needs y");
+    if (model == FM_UBCM && y) return fail(FM_ERR_INVALID, "UBCM takes no y");
+    if (seg_target == 0) seg_target = 256;
+    if (seg_target < 8 || seg_target > (int64_t(1) << 40))
+        return fail(FM_ERR_INVALID, "seg_target %lld outside [8, 2^40]", (long long)seg_target);
+
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int dev = 0;
+    CK(cudaGetDevice(&dev), "cudaGetDevice");
+    configure_pool_once(dev);
+    Allocs tmp(st);
+
+    // ---- inputs: host or device ----
+    const double *xd = x, *yd = y;
+    if (!is_device_ptr(x)) {
+        double *t;
+        CK(tmp.get(&t, n), "alloc x");
+        CK(cudaMemcpyAsync(t, x, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy x");
+        xd = t;
+    }
+    if (model == FM_ECM && !is_device_ptr(y)) {
+        double *t;
+        CK(tmp.get(&t, n), "alloc y");
+        CK(cudaMemcpyAsync(t, y, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy y");
+        yd = t;
+    }
+
+    // ---- a1: validate + key ----
+    uint64_t *ka, *kb;
+    int32_t *ia, *ib;
+    PlanScalars *sc;
+    CK(tmp.get(&ka, n), "alloc keys");
+    CK(tmp.get(&kb, n), "alloc keys");
+    CK(tmp.get(&ia, n), "alloc ids");
+    CK(tmp.get(&ib, n), "alloc ids");
+    CK(tmp.get(&sc, 1), "alloc scalars");
+    PlanScalars h_sc;
+    memset(&h_sc, 0, sizeof(h_sc));
+    h_sc.key_and = ~0ull;
+    CK(cudaMemcpyAsync(sc, &h_sc, sizeof(h_sc), cudaMemcpyHostToDevice, st), "init scalars");
+    k_validate_key<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, xd, yd, ka, ia, sc);
+    CK(cudaGetLastError(), "k_validate_key");
+    CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
+    CK(cudaStreamSynchronize(st), "sync (validate)");
+    if (h_sc.flags & kErrInvalid)
+        return fail(FM_ERR_INVALID, "invalid fitness: x must be finite >= 0, y in [0,1), kappa_max^2 finite");
+
+    Plan *p = new Plan();
+    memset(p, 0, sizeof(Plan));
+    p->magic = kPlanMagic;
+    p->model = (int)model;
+    p->n = n;
+    p->S = seg_target;
+    p->device = dev;
+    struct PlanGuard {
+        Plan *p;
+        ~PlanGuard() { if (p) plan_release(p); }
+    } guard{p};
+
+    // ---- a2: sort ----
+    size_t tmp_bytes = std::max(radix_tmp_bytes(n), scan_tmp_bytes(n + 1) + 256);
+    void *work;
+    CK(tmp.get((char **)&work, tmp_bytes), "alloc sort tmp");
+    uint64_t *skeys;
+    int32_t *perm;
+    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, (uint64_t)(h_sc.key_or ^ h_sc.key_and), &skeys, &perm, work, tmp_bytes,
+                          st),
+       "radix sort");
+    tmp.release(perm);
+    p->perm = perm;  // adopt the sorted id buffer (freed by plan_release via cudaFree)
+    CK(cudaMallocAsync((void **)&p->kappa_s, sizeof(double) * n, st), "alloc kappa_s");
+    if (model == FM_ECM) {
+        CK(cudaMallocAsync((void **)&p->y_s, sizeof(double) * n, st), "alloc y_s");
+        CK(cudaMallocAsync((void **)&p->ymax, sizeof(double) * (n + 1), st), "alloc ymax");
+    }
+    k_gather_sorted<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, skeys, yd, p->perm, p->kappa_s, p->y_s);
+    CK(cudaGetLastError(), "k_gather_sorted");
+
+    // ---- a3: suffix max of y (beta_min) ----
+    if (model == FM_ECM) CK(suffix_max_f64(p->y_s, p->ymax, n, work, tmp_bytes, st), "suffix max");
+
+    // ---- a4: planner ----
+    uint64_t *P;
+    RowInfo *rows;
+    int64_t *row_m;
+    CK(tmp.get(&P, n + 1), "alloc P");
+    CK(tmp.get(&rows, n), "alloc rows");
+    CK(tmp.get(&row_m, n + 1), "alloc row_m");
+    k_set_F<<<1, 1, 0, st>>>(n, ceil_log2(n), p->kappa_s, sc);
+    k_kfx<<<grid_for(n, 256), 256, 0, st>>>(n, p->kappa_s, sc, P);
+    CK(cudaGetLastError(), "k_kfx");
+    CK(scan_exclusive_u64(P, P, n, work, tmp_bytes, st), "scan P");
+    k_rows<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, seg_target, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
+                                             row_m);
+    CK(cudaGetLastError(), "k_rows");
+    CK(scan_exclusive_i64(row_m, row_m, n, work, tmp_bytes, st), "scan rows");
+    int64_t n_seg = 0;
+    CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
+    CK(cudaMemcpyAsync(&n_seg, row_m + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "read n_seg");
+    CK(cudaStreamSynchronize(st), "sync (rows)");
+    p->F = h_sc.F;
+    p->n_seg = n_seg;
+    p->wmax = h_sc.wmax;
+    p->est_draws = h_sc.total_work >> kG;
+    // row_m now holds row_seg (exclusive prefix of the per-row segment counts, n+1 entries)
+    CK(cudaMallocAsync((void **)&p->seg, sizeof(int4) * std::max<int64_t>(n_seg, 1), st), "alloc seg");
+    CK(cudaMallocAsync((void **)&p->seg_h0, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_h0");
+    CK(cudaMallocAsync((void **)&p->seg_q0, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_q0");
+    CK(cudaMallocAsync((void **)&p->seg_omT, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_omT");
+    int64_t *seg_work;
+    CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
+    k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n, n_seg, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
+                                                 row_m, p->seg, p->seg_h0, p->seg_q0, p->seg_omT, seg_work);
+    CK(cudaGetLastError(), "k_emit");
+    {
+        const size_t wb = scan_tmp_bytes(n_seg + 1);
+        char *work2;
+        CK(tmp.get(&work2, wb), "alloc scan tmp");
+        CK(scan_exclusive_i64(seg_work, seg_work, n_seg, work2, wb, st), "scan work");
+    }
+
+    // ---- chunking (never changes results) ----
+    const int64_t lane_draws = std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 256));
+    const int64_t target = 32 * lane_draws * kUnit;
+    const int64_t total = h_sc.total_work;
+    p->chunk_target = target;
+    p->n_chunks = std::max<int64_t>(1, (total + target - 1) / target);
+    CK(cudaMallocAsync((void **)&p->chunk_seg, sizeof(int64_t) * (p->n_chunks + 1), st), "alloc chunks");
+    k_chunks<<<grid_for(p->n_chunks + 1, 256), 256, 0, st>>>(n_seg, p->n_chunks, target, seg_work, p->chunk_seg);
+    CK(cudaGetLastError(), "k_chunks");
+    // scratch slot per task: chunk work < target + wmax (DESIGN 7.2); edges <= draws
+    const double est = (double)(target + p->wmax) / (double)kUnit;
+    p->cap = (int64_t)(est * 1.25) + 256;
+    const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
+    if (cap_override > 0) p->cap = cap_override;
+
+    CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
+    CK(cudaStreamSynchronize(st), "sync (plan)");
+    if (h_sc.flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
+
+    guard.p = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_plans.insert(p);
+    }
+    *plan_out = (fm_plan *)p;
+    return FM_OK;
+}
+
+static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                             void *cuda_stream, fm_edges *out)
+{
+    if (!out) return fail(FM_ERR_INVALID, "out is NULL");
+    memset(out, 0, sizeof(*out));
+    if (!plan_ || !plan_live(plan_)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan_;
+    if (p->model != model)
+        return fail(FM_ERR_STATE, "plan model %s used with fm_sample_%s", p->model == FM_UBCM ? "UBCM" : "ECM",
+                    model == FM_UBCM ? "ubcm" : "ecm");
+    if (n_samples < 0 || first_sample < 0 || first_sample + n_samples > (int64_t(1) << 32))
+        return fail(FM_ERR_INVALID, "sample range [%lld, +%lld) outside [0, 2^32)", (long long)first_sample,
+                    (long long)n_samples);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    Allocs tmp(st);
+
+    int64_t *offsets_h = (int64_t *)calloc((size_t)n_samples + 1, sizeof(int64_t));
+    Owner *own = new Owner();
+    memset(own, 0, sizeof(Owner));
+    own->magic = kOwnerMagic;
+    own->offsets_host = offsets_h;
+    own->stream = st;
+    struct OwnGuard {
+        Owner *o;
+        ~OwnGuard()
+        {
+            if (o) {
+                free(o->offsets_host);
+                if (o->edges) cudaFreeAsync(o->edges, o->stream);
+                if (o->weights) cudaFreeAsync(o->weights, o->stream);
+                delete o;
+            }
+        }
+    } og{own};
+    if (!offsets_h) return fail(FM_ERR_NOMEM, "host offsets");
+
+    const int64_t n_tasks = n_samples * p->n_chunks;
+    struct Hdr {
+        unsigned long long counters[3];
+        unsigned int flags;
+        unsigned int pad;
+        unsigned long long n_overflow;
+    };
+    Hdr h;
+    memset(&h, 0, sizeof(h));
+    if (n_tasks > 0) {
+        int2 *se;
+        int32_t *sw = nullptr;
+        int64_t *counts, *dest, *ovl, *offs_d;
+        Hdr *hd;
+        const int64_t slots = n_tasks * p->cap;
+        CK(tmp.get(&se, slots), "alloc scratch edges");
+        if (model == FM_ECM) CK(tmp.get(&sw, slots), "alloc scratch weights");
+        CK(tmp.get(&counts, n_tasks + 1), "alloc counts");
+        CK(tmp.get(&dest, n_tasks + 1), "alloc dest");
+        CK(tmp.get(&ovl, n_tasks), "alloc overflow list");
+        CK(tmp.get(&offs_d, n_samples + 1), "alloc offsets");
+        CK(tmp.get(&hd, 1), "alloc hdr");
+        const size_t stb = scan_tmp_bytes(n_tasks + 1);
+        char *scan_tmp;
+        CK(tmp.get(&scan_tmp, stb), "alloc scan tmp");
+        CK(cudaMemsetAsync(hd, 0, sizeof(Hdr), st), "memset hdr");
+
+        SampleArgs a;
+        memset(&a, 0, sizeof(a));
+        a.seg = p->seg;
+        a.seg_h0 = p->seg_h0;
+        a.seg_q0 = p->seg_q0;
+        a.seg_omT = p->seg_omT;
+        a.kappa_s = p->kappa_s;
+        a.y_s = p->y_s;
+        a.perm = p->perm;
+        a.chunk_seg = p->chunk_seg;
+        a.n_chunks = p->n_chunks;
+        a.cap = p->cap;
+        a.k0 = (uint32_t)(seed & 0xffffffffu);
+        a.k1 = (uint32_t)(seed >> 32);
+        a.first_sample = (uint32_t)first_sample;
+        a.n_tasks = n_tasks;
+        a.edges = se;
+        a.weights = sw;
+        a.counts = counts;
+        a.counters = hd->counters;
+        a.flags = &hd->flags;
+        CK(launch_sample(model, a, st), "sampler launch");
+        CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
+        CK(launch_offsets(n_samples, p->n_chunks, dest, offs_d, st), "offsets");
+        CK(launch_overflow(n_tasks, p->cap, counts, &hd->n_overflow, ovl, st), "overflow check");
+        CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
+           "read offsets");
+        CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+        CK(cudaStreamSynchronize(st), "sync (sample)");
+        const int64_t total = offsets_h[n_samples];
+        CK(cudaMallocAsync(&own->edges, sizeof(int2) * std::max<int64_t>(total, 1), st), "alloc edges");
+        if (model == FM_ECM)
+            CK(cudaMallocAsync(&own->weights, sizeof(int32_t) * std::max<int64_t>(total, 1), st), "alloc weights");
+        CK(launch_compact(n_tasks, p->cap, counts, dest, se, sw, (int2 *)own->edges, (int32_t *)own->weights, st),
+           "compact");
+        if (h.n_overflow) {  // deterministic re-run of overflowed chunks straight into the final array
+            SampleArgs r = a;
+            r.n_tasks = (int64_t)h.n_overflow;
+            r.task_list = ovl;
+            r.rerun_base = dest;
+            r.edges = (int2 *)own->edges;
+            r.weights = (int32_t *)own->weights;
+            CK(launch_sample(model, r, st), "rerun launch");
+        }
+        out->n_edges = total;
+    }
+    out->n_samples = n_samples;
+    out->offsets = offsets_h;
+    out->edges = (int32_t *)own->edges;
+    out->weights = (int32_t *)own->weights;
+    out->draws = (int64_t)h.counters[0];
+    out->landed = (int64_t)h.counters[1];
+    out->accepted = (int64_t)h.counters[2];
+    out->segments = p->n_seg * n_samples;
+    out->chunks = n_tasks;
+    out->flags = ((h.flags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u) |
+                 (h.n_overflow ? FM_FLAG_SCRATCH_RERUN : 0u);
+    out->_owner = own;
+    og.o = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_owners.insert(own);
+    }
+    if (h.flags & kErrBound) return fail(FM_ERR_BOUND, "p > q detected");
+    return FM_OK;
+}
+
+fm_status fm_sample_ubcm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                         void *cuda_stream, fm_edges *out)
+{
+    return sample_impl(FM_UBCM, plan, seed, first_sample, n_samples, cuda_stream, out);
+}
+
+fm_status fm_sample_ecm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                        void *cuda_stream, fm_edges *out)
+{
+    return sample_impl(FM_ECM, plan, seed, first_sample, n_samples, cuda_stream, out);
+}
+
+fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host, void *cuda_stream)
+{
+    if (!e) return fail(FM_ERR_INVALID, "NULL result");
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_owners.count(e->_owner)) return fail(FM_ERR_STATE, "not a live fm_edges");
+    }
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (e->n_edges > 0) {
+        if (!edges_host) return fail(FM_ERR_INVALID, "edges_host is NULL");
+        CK(cudaMemcpyAsync(edges_host, e->edges, sizeof(int32_t) * 2 * e->n_edges, cudaMemcpyDeviceToHost, st),
+           "copy edges");
+        if (weights_host && e->weights)
+            CK(cudaMemcpyAsync(weights_host, e->weights, sizeof(int32_t) * e->n_edges, cudaMemcpyDeviceToHost, st),
+               "copy weights");
+    }
+    CK(cudaStreamSynchronize(st), "sync (to_host)");
+    return FM_OK;
+}
+
+fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info)
+{
+    if (!info) return fail(FM_ERR_INVALID, "info is NULL");
+    if (!plan || !plan_live(plan)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan;
+    info->model = p->model;
+    info->n = p->n;
+    info->seg_target = p->S;
+    info->F = p->F;
+    info->n_segments = p->n_seg;
+    info->n_chunks = p->n_chunks;
+    info->est_draws = p->est_draws;
+    return FM_OK;
+}
+
+fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax, int32_t *seg,
+                         double *seg_h0, double *seg_q0, double *seg_omT)
+{
+    if (!plan || !plan_live(plan)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan;
+    CK(cudaDeviceSynchronize(), "sync");
+    const size_t n = (size_t)p->n, s = (size_t)p->n_seg;
+    if (perm) CK(cudaMemcpy(perm, p->perm, n * 4, cudaMemcpyDeviceToHost), "perm");
+    if (kappa_s) CK(cudaMemcpy(kappa_s, p->kappa_s, n * 8, cudaMemcpyDeviceToHost), "kappa_s");
+    if (y_s && p->y_s) CK(cudaMemcpy(y_s, p->y_s, n * 8, cudaMemcpyDeviceToHost), "y_s");
+    if (ymax && p->ymax) CK(cudaMemcpy(ymax, p->ymax, (n + 1) * 8, cudaMemcpyDeviceToHost), "ymax");
+    if (seg && s) CK(cudaMemcpy(seg, p->seg, s * 16, cudaMemcpyDeviceToHost), "seg");
+    if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->seg_h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
+    if (seg_q0 && s) CK(cudaMemcpy(seg_q0, p->seg_q0, s * 8, cudaMemcpyDeviceToHost), "seg_q0");
+    if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->seg_omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
+    return FM_OK;
+}
+
+void fm_free(void *obj)
+{
+    if (!obj) return;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (g_plans.erase(obj)) {
+            cudaDeviceSynchronize();
+            plan_release((Plan *)obj);
+            return;
+        }
+    }
+    fm_edges *e = (fm_edges *)obj;
+    Owner *o = (Owner *)e->_owner;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!o || !g_owners.erase(o)) return;  // not ours: ignore
+    }
+    if (o->edges) cudaFreeAsync(o->edges, o->stream);
+    if (o->weights) cudaFreeAsync(o->weights, o->stream);
+    free(o->offsets_host);
+    o->magic = 0;
+    delete o;
+    memset(e, 0, sizeof(*e));
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// fm_internal.cuh -- internal definitions shared by the CUDA translation units of the product
+// library (NOT shared with oracle/).  sm_100a only.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fastmaxent.h"
+
+namespace fm {
+
+constexpr int kG = 16;                         // work unit: one expected draw = 2^G (DESIGN 3.4)
+constexpr int64_t kUnit = int64_t(1) << kG;
+constexpr uint32_t kPlanMagic = 0x4C504D46u;   // "FMPL"
+constexpr uint32_t kOwnerMagic = 0x57504D46u;  // "FMPW"
+
+// device-side error flags (atomicOr)
+enum : uint32_t {
+    kErrInvalid = 1u,     // a1 validation failed
+    kErrState = 2u,       // planner invariant violated (cuts not strictly increasing)
+    kErrBound = 4u,       // p > q (1 + 2^-50)
+    kFlagWeightSat = 8u,  // ECM weight clamped
+};
+
+struct Plan {
+    uint32_t magic;
+    int model;
+    int64_t n, S;
+    int F;
+    int device;
+    // a2/a3 (rank space)
+    int32_t *perm;      // [n] rank -> id
+    double *kappa_s;    // [n]
+    double *y_s;        // [n] ECM
+    double *ymax;       // [n+1] ECM
+    // a4 segments
+    int64_t n_seg;
+    int4 *seg;          // [n_seg] (u, a, b, sigma)
+    double *seg_h0;     // [n_seg]
+    double *seg_q0;     // [n_seg]
+    double *seg_omT;    // [n_seg] ECM (1.0 for UBCM)
+    int64_t est_draws;  // sum of segment work estimates / 2^G
+    // chunking (does not change results)
+    int64_t n_chunks;
+    int64_t *chunk_seg;   // [n_chunks+1] first segment of each chunk
+    int64_t chunk_target; // work per chunk (units 2^G)
+    int64_t wmax;         // bound of one segment's work (units 2^G)
+    int64_t cap;          // scratch slot per (sample, chunk), edges
+};
+
+struct Owner {
+    uint32_t magic;
+    void *edges;    // device
+    void *weights;  // device
+    int64_t *offsets_host;
+    cudaStream_t stream;
+};
+
+// ------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11) -- DESIGN.md R1.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// u01(k) = (k + 0.5) 2^-32 (R2); both operations exact
+__device__ __forceinline__ double u01(uint32_t k)
+{
+    return __dmul_rn(__dadd_rn((double)k, 0.5), 0x1p-32);
+}
+
+// ------------------------------------------------------------------------------------------
+// launch helpers (fm_scan.cu)
+// ------------------------------------------------------------------------------------------
+// exclusive prefix sum of int64 in[0..n) -> out[0..n], out[n] = total.  in == out allowed.
+cudaError_t scan_exclusive_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
+                               cudaStream_t st);
+size_t scan_tmp_bytes(int64_t n);
+// same for uint64
+cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
+                               cudaStream_t st);
+// reverse inclusive max: out[t] = max(in[t], out[t+1]), out[n] = 0.0 (out has n+1 entries)
+cudaError_t suffix_max_f64(const double *in, double *out, int64_t n, void *tmp, size_t tmp_bytes,
+                           cudaStream_t st);
+
+// radix sort (fm_sort.cu): sort (key, val) pairs ascending by key, stable.  Buffers are
+// ping-ponged; on return *key_out/*val_out point to the sorted arrays (one of the two buffers).
+// vary_bits: OR of (key ^ key0) over all keys -- digits with no varying bit are skipped.
+cudaError_t radix_sort_u64_i32(uint64_t *keys_a, uint64_t *keys_b, int32_t *vals_a, int32_t *vals_b, int64_t n,
+                               uint64_t vary_bits, uint64_t **key_out, int32_t **val_out, void *tmp,
+                               size_t tmp_bytes, cudaStream_t st);
+size_t radix_tmp_bytes(int64_t n);
+
+}  // namespace fm

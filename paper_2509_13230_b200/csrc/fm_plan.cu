@@ -1,0 +1,203 @@
+// fm_plan.cu -- a1 (validate + key), a2 gathers, a3 (beta_min suffix max), a4 (planner).
+// Every floating-point operation on the planner path is an explicit round-to-nearest
+// intrinsic in the order of DESIGN.md section 3.4, so the plan is bit-identical to the
+// oracle's (compiled with --fmad=false as a second guard).
+#include <float.h>
+
+#include "fm_internal.cuh"
+#include "fm_plan_kernels.cuh"
+
+namespace fm {
+
+// ------------------------------------------------------------------------------------------
+// a1: validate (x finite >= 0; ECM y in [0,1); kappa^2 finite) and build the radix key
+// ~bits(kappa) (kappa = x or x*y; -0.0 normalised to +0.0).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, const double *__restrict__ x,
+                                                      const double *__restrict__ y, uint64_t *__restrict__ keys,
+                                                      int32_t *__restrict__ ids, PlanScalars *sc)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t kor = 0, kand = ~0ull;
+    bool bad = false;
+    if (i < n) {
+        const double xi = x[i];
+        bool ok = isfinite(xi) && xi >= 0.0;
+        double kappa = xi;
+        if (model == FM_ECM) {
+            const double yi = y[i];
+            ok = ok && isfinite(yi) && yi >= 0.0 && yi < 1.0;
+            kappa = __dmul_rn(xi, yi);
+        }
+        kappa = __dadd_rn(kappa, 0.0);  // -0.0 -> +0.0
+        ok = ok && isfinite(__dmul_rn(kappa, kappa));
+        const uint64_t key = ~(uint64_t)__double_as_longlong(kappa);
+        keys[i] = key;
+        ids[i] = (int32_t)i;
+        kor = key;
+        kand = key;
+        bad = !ok;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+        kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+    }
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+        atomicOr(&sc->key_or, (unsigned long long)kor);
+        atomicAnd(&sc->key_and, (unsigned long long)kand);
+        if (anybad) atomicOr(&sc->flags, kErrInvalid);
+    }
+}
+
+// a2 epilogue: rank-space arrays from the sorted keys
+__global__ void __launch_bounds__(256) k_gather_sorted(int model, int64_t n, const uint64_t *__restrict__ skeys,
+                                                       const double *__restrict__ y, const int32_t *__restrict__ perm,
+                                                       double *__restrict__ kappa_s, double *__restrict__ y_s)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    kappa_s[r] = __longlong_as_double((long long)~skeys[r]);
+    if (model == FM_ECM) y_s[r] = y[perm[r]];
+}
+
+// a4 step 1-2: F and the fixed-point keys
+__global__ void k_set_F(int64_t n, int L, const double *kappa_s, PlanScalars *sc)
+{
+    int e = 0;
+    const double k0 = kappa_s[0];
+    if (k0 > 0.0) frexp(k0, &e);
+    sc->F = 61 - e - L;
+}
+
+__global__ void __launch_bounds__(256) k_kfx(int64_t n, const double *__restrict__ kappa_s,
+                                             const PlanScalars *__restrict__ sc, uint64_t *__restrict__ kfx)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    kfx[v] = (uint64_t)floor(ldexp(kappa_s[v], sc->F));
+}
+
+// a4 step 3-4 (per row): r_u, sat_u, Wtot_u, m_u
+__global__ void __launch_bounds__(256) k_rows(int model, int64_t n, int64_t S, const double *__restrict__ kappa_s,
+                                              const double *__restrict__ y_s, const double *__restrict__ ymax,
+                                              const uint64_t *__restrict__ P, PlanScalars *sc, RowInfo *__restrict__ rows,
+                                              int64_t *__restrict__ row_m)
+{
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long work = 0;
+    if (u < n - 1) {
+        const int F = sc->F;
+        double r = kappa_s[u];
+        if (model == FM_ECM) r = __ddiv_rn(kappa_s[u], __dsub_rn(1.0, __dmul_rn(y_s[u], ymax[u + 1])));
+        int64_t sat;
+        if (__dmul_rn(r, kappa_s[u + 1]) < 1.0) {
+            sat = u + 1;
+        } else {  // smallest v in [u+1, n] with v == n or r*kappa_s[v] < 1 (monotone predicate)
+            int64_t lo = u + 2, hi = n;
+            while (lo < hi) {
+                const int64_t mid = lo + ((hi - lo) >> 1);
+                if (__dmul_rn(r, kappa_s[mid]) < 1.0) hi = mid; else lo = mid + 1;
+            }
+            sat = lo;
+        }
+        const int64_t WN = plan_W(P, F, u, r, sat, n);
+        const int64_t Wt = WN + kUnit;
+        const int64_t m = (Wt + S * kUnit - 1) / (S * kUnit);
+        rows[u].r = r;
+        rows[u].sat = sat;
+        rows[u].wtot = Wt;
+        row_m[u] = m;
+        work = WN + m * kUnit;
+        // bound of one segment's work: Wtot (unsplit) or ceil(Wtot/m) + 2 units + 2 (DESIGN 7.2)
+        const int64_t wseg = m == 1 ? Wt : (Wt + m - 1) / m + 2 * kUnit + 2;
+        atomicMax(&sc->wmax, (long long)wseg);
+    } else if (u == n - 1) {
+        row_m[u] = 0;
+    }
+    // block reduce of work (int64)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
+    if ((threadIdx.x & 31) == 0 && work) atomicAdd((unsigned long long *)&sc->total_work, (unsigned long long)work);
+}
+
+// cut k of row u (1 <= k < m): smallest v in [u+2, n-1] with W_u(v) >= floor(k Wtot / m), n-1 if none
+__device__ __forceinline__ int64_t plan_cut(const uint64_t *P, int F, int64_t n, int64_t u, const RowInfo &ri,
+                                            int64_t m, int64_t k)
+{
+    const int64_t q = ri.wtot / m, rm = ri.wtot - q * m;
+    const int64_t theta = k * q + (k * rm) / m;  // == floor(k * Wtot / m) exactly
+    int64_t lo = u + 2, hi = n - 1;
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (plan_W(P, F, u, ri.r, ri.sat, mid) >= theta) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// a4 step 5-6 (per segment): (u, a, b, sigma), initial bound (q0, h0, omT), work estimate
+__global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_seg, const double *__restrict__ kappa_s,
+                                              const double *__restrict__ y_s, const double *__restrict__ ymax,
+                                              const uint64_t *__restrict__ P, PlanScalars *sc,
+                                              const RowInfo *__restrict__ rows, const int64_t *__restrict__ row_seg,
+                                              int4 *__restrict__ seg,
+                                              double *__restrict__ seg_h0, double *__restrict__ seg_q0,
+                                              double *__restrict__ seg_omT, int64_t *__restrict__ seg_work)
+{
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_seg) return;
+    const int F = sc->F;
+    // row u: largest u with row_seg[u] <= g; u in [g - extra, g] since every row u < n-1 has >= 1 segment
+    const int64_t extra = n_seg - (n - 1);
+    int64_t lo = g - extra > 0 ? g - extra : 0, hi = g < n - 2 ? g : n - 2;
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo + 1) >> 1);
+        if (row_seg[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const int64_t u = lo;
+    const int64_t sigma = g - row_seg[u];
+    const int64_t m = row_seg[u + 1] - row_seg[u];
+    const RowInfo ri = rows[u];
+    int64_t a, b;
+    a = sigma == 0 ? u + 1 : plan_cut(P, F, n, u, ri, m, sigma);
+    b = sigma == m - 1 ? n : plan_cut(P, F, n, u, ri, m, sigma + 1);
+    if (!(a < b) || !(a > u)) atomicOr(&sc->flags, kErrState);
+    seg[g] = make_int4((int)u, (int)a, (int)b, (int)sigma);
+    const double kq = __dmul_rn(kappa_s[u], kappa_s[a - 1]);
+    if (model == FM_UBCM) {
+        seg_omT[g] = 1.0;
+        seg_q0[g] = __ddiv_rn(kq, __dadd_rn(1.0, kq));
+        seg_h0[g] = log1p(kq);
+    } else {
+        const double T = __dmul_rn(y_s[u], ymax[a]);
+        const double omT = __dsub_rn(1.0, T);
+        seg_omT[g] = omT;
+        seg_q0[g] = __ddiv_rn(kq, __dadd_rn(omT, kq));
+        seg_h0[g] = log1p(__ddiv_rn(kq, omT));
+    }
+    const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, u, ri.r, ri.sat, a);
+    const int64_t wb = plan_W(P, F, u, ri.r, ri.sat, b);
+    seg_work[g] = wb - wa + kUnit;
+}
+
+// chunking: chunk c starts at the first segment whose work prefix reaches c * target
+__global__ void __launch_bounds__(256) k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target,
+                                                const int64_t *__restrict__ work_pre, int64_t *__restrict__ chunk_seg)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c > n_chunks) return;
+    if (c == n_chunks) {
+        chunk_seg[c] = n_seg;
+        return;
+    }
+    const int64_t th = c * target;
+    int64_t lo = 0, hi = n_seg;  // smallest g with work_pre[g] >= th
+    while (lo < hi) {
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (work_pre[mid] >= th) hi = mid; else lo = mid + 1;
+    }
+    chunk_seg[c] = lo;
+}
+
+}  // namespace fm

@@ -1,0 +1,81 @@
+// fm_plan_kernels.cuh -- planner kernels (fm_plan.cu) and sampler kernels (fm_sample.cu),
+// declared for the host orchestration in fm_capi.cu.
+#pragma once
+#include "fm_internal.cuh"
+
+namespace fm {
+
+struct PlanScalars {
+    unsigned long long key_or;
+    unsigned long long key_and;
+    unsigned int flags;
+    int F;
+    long long total_work;  // sum over segments of work estimates (units 2^G)
+    long long wmax;        // upper bound of any one segment's work (units 2^G)
+};
+
+struct RowInfo {
+    double r;      // row multiplier r_u
+    int64_t sat;   // saturation index sat_u
+    int64_t wtot;  // Wtot_u
+};
+
+// W_u(v) (DESIGN.md 3.4 step 3): integer estimate of the draws over candidates [u+1, v)
+__device__ __forceinline__ int64_t plan_W(const uint64_t *P, int F, int64_t u, double r, int64_t sat, int64_t v)
+{
+    const int64_t vs = v < sat ? v : sat;
+    int64_t W = (vs - u - 1) * kUnit;
+    if (v > sat) {
+        const uint64_t D = P[v] - P[sat];
+        W += (int64_t)floor(ldexp(__dmul_rn(r, __ull2double_rn(D)), kG - F));
+    }
+    return W;
+}
+
+__global__ void k_validate_key(int model, int64_t n, const double *x, const double *y, uint64_t *keys, int32_t *ids,
+                               PlanScalars *sc);
+__global__ void k_gather_sorted(int model, int64_t n, const uint64_t *skeys, const double *y, const int32_t *perm,
+                                double *kappa_s, double *y_s);
+__global__ void k_set_F(int64_t n, int L, const double *kappa_s, PlanScalars *sc);
+__global__ void k_kfx(int64_t n, const double *kappa_s, const PlanScalars *sc, uint64_t *kfx);
+__global__ void k_rows(int model, int64_t n, int64_t S, const double *kappa_s, const double *y_s, const double *ymax,
+                       const uint64_t *P, PlanScalars *sc, RowInfo *rows, int64_t *row_m);
+__global__ void k_emit(int model, int64_t n, int64_t n_seg, const double *kappa_s, const double *y_s,
+                       const double *ymax, const uint64_t *P, PlanScalars *sc, const RowInfo *rows,
+                       const int64_t *row_seg, int4 *seg, double *seg_h0, double *seg_q0, double *seg_omT,
+                       int64_t *seg_work);
+__global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg);
+
+// ------------------------------------------------------------------------------------------
+// sampler (fm_sample.cu)
+// ------------------------------------------------------------------------------------------
+struct SampleArgs {
+    const int4 *seg;
+    const double *seg_h0, *seg_q0, *seg_omT;
+    const double *kappa_s, *y_s;
+    const int32_t *perm;
+    const int64_t *chunk_seg;
+    int64_t n_chunks;
+    int64_t cap;                // scratch slot per task (edges)
+    uint32_t k0, k1;
+    uint32_t first_sample;
+    int64_t n_tasks;            // warps launched
+    const int64_t *task_list;   // NULL: task = warp index; else task_list[warp]
+    int2 *edges;                // scratch (normal) or final array (rerun)
+    int32_t *weights;           // ECM
+    const int64_t *rerun_base;  // rerun mode: per-task output base (final offsets); NULL otherwise
+    int64_t *counts;            // [n_samples * n_chunks] edges produced per task (normal mode)
+    unsigned long long *counters;  // draws, landed, accepted
+    unsigned int *flags;
+};
+
+cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st);
+// tasks whose count exceeds the slot -> overflow list (re-run straight into the final array)
+cudaError_t launch_overflow(int64_t n_tasks, int64_t cap, const int64_t *counts, unsigned long long *n_overflow,
+                            int64_t *overflow_list, cudaStream_t st);
+cudaError_t launch_compact(int64_t n_tasks, int64_t cap, const int64_t *counts, const int64_t *dest,
+                           const int2 *scratch_e, const int32_t *scratch_w, int2 *out_e, int32_t *out_w,
+                           cudaStream_t st);
+cudaError_t launch_offsets(int64_t n_samples, int64_t n_chunks, const int64_t *dest, int64_t *offsets, cudaStream_t st);
+
+}  // namespace fm

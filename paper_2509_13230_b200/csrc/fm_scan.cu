@@ -1,0 +1,174 @@
+// fm_scan.cu -- device scans used by the planner and the output writer (a4, a6).
+// Reduce-then-scan in three launches: per-tile reduction, one-block scan of tile partials,
+// per-tile scan seeded by its partial.  Tiles are 256 threads x 8 contiguous items.
+#include "fm_internal.cuh"
+
+namespace fm {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 8;
+constexpr int kTile = kThreads * kItems;
+
+struct SumI64 {
+    using T = int64_t;
+    __device__ static T id() { return 0; }
+    __device__ static T op(T a, T b) { return a + b; }
+};
+struct SumU64 {
+    using T = uint64_t;
+    __device__ static T id() { return 0; }
+    __device__ static T op(T a, T b) { return a + b; }
+};
+struct MaxF64 {
+    using T = double;
+    __device__ static T id() { return 0.0; }  // inputs are >= 0 (y in [0,1))
+    __device__ static T op(T a, T b) { return fmax(a, b); }
+};
+
+// logical index i -> physical index (reverse scans walk the array from the end)
+template <bool kRev>
+__device__ __forceinline__ int64_t phys(int64_t i, int64_t n) { return kRev ? n - 1 - i : i; }
+
+template <typename Op>
+__device__ __forceinline__ typename Op::T block_exclusive(typename Op::T v, typename Op::T *total)
+{
+    using T = typename Op::T;
+    __shared__ T warp_tot[kThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = Op::op(t, inc);
+    }
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    T wpre = Op::id(), all = Op::id();
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; w++) {
+        if (w < wid) wpre = Op::op(wpre, warp_tot[w]);
+        all = Op::op(all, warp_tot[w]);
+    }
+    T exc = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) exc = Op::id();
+    __syncthreads();
+    *total = all;
+    return Op::op(wpre, exc);
+}
+
+template <typename Op, bool kRev>
+__global__ void __launch_bounds__(kThreads) k_tile_reduce(const typename Op::T *in, int64_t n,
+                                                          typename Op::T *partial)
+{
+    using T = typename Op::T;
+    const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    T acc = Op::id();
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = base + k;
+        if (i < n) acc = Op::op(acc, in[phys<kRev>(i, n)]);
+    }
+    T tot;
+    block_exclusive<Op>(acc, &tot);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// one block: exclusive scan of partial[0..nb) in place
+template <typename Op>
+__global__ void __launch_bounds__(kThreads) k_partials(typename Op::T *partial, int64_t nb)
+{
+    using T = typename Op::T;
+    T carry = Op::id();
+    for (int64_t b0 = 0; b0 < nb; b0 += kTile) {
+        T v[kItems];
+        T acc = Op::id();
+#pragma unroll
+        for (int k = 0; k < kItems; k++) {
+            const int64_t i = b0 + (int64_t)threadIdx.x * kItems + k;
+            v[k] = i < nb ? partial[i] : Op::id();
+            acc = Op::op(acc, v[k]);
+        }
+        T tot;
+        T pre = Op::op(carry, block_exclusive<Op>(acc, &tot));
+#pragma unroll
+        for (int k = 0; k < kItems; k++) {
+            const int64_t i = b0 + (int64_t)threadIdx.x * kItems + k;
+            if (i < nb) partial[i] = pre;
+            pre = Op::op(pre, v[k]);
+        }
+        carry = Op::op(carry, tot);
+        __syncthreads();
+    }
+}
+
+// kInclusive=false: out[i] = op(in[0..i)), out[n] = total.  true: out[i] = op(in[0..i]).
+template <typename Op, bool kRev, bool kInclusive>
+__global__ void __launch_bounds__(kThreads) k_tile_scan(const typename Op::T *in, typename Op::T *out, int64_t n,
+                                                        const typename Op::T *partial, int64_t nb)
+{
+    using T = typename Op::T;
+    const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)threadIdx.x * kItems;
+    T v[kItems];
+    T acc = Op::id();
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = base + k;
+        v[k] = i < n ? in[phys<kRev>(i, n)] : Op::id();
+        acc = Op::op(acc, v[k]);
+    }
+    T tot;
+    T pre = Op::op(partial[blockIdx.x], block_exclusive<Op>(acc, &tot));
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = base + k;
+        if (kInclusive) pre = Op::op(pre, v[k]);
+        if (i < n) out[phys<kRev>(i, n)] = pre;
+        if (!kInclusive) pre = Op::op(pre, v[k]);
+    }
+    if (!kInclusive && blockIdx.x == nb - 1 && threadIdx.x == kThreads - 1) out[n] = pre;
+}
+
+template <typename Op, bool kRev, bool kInclusive>
+cudaError_t run_scan(const typename Op::T *in, typename Op::T *out, int64_t n, void *tmp, size_t tmp_bytes,
+                     cudaStream_t st)
+{
+    using T = typename Op::T;
+    if (n <= 0) return cudaSuccess;
+    const int64_t nb = (n + kTile - 1) / kTile;
+    if (tmp_bytes < sizeof(T) * (size_t)nb) return cudaErrorInvalidValue;
+    T *partial = (T *)tmp;
+    k_tile_reduce<Op, kRev><<<(unsigned)nb, kThreads, 0, st>>>(in, n, partial);
+    k_partials<Op><<<1, kThreads, 0, st>>>(partial, nb);
+    k_tile_scan<Op, kRev, kInclusive><<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, partial, nb);
+    return cudaGetLastError();
+}
+
+__global__ void k_set_f64(double *p, double v) { *p = v; }
+
+}  // namespace
+
+size_t scan_tmp_bytes(int64_t n) { return sizeof(int64_t) * (size_t)((n + kTile - 1) / kTile + 1); }
+
+cudaError_t scan_exclusive_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
+                               cudaStream_t st)
+{
+    if (n == 0) return cudaMemsetAsync(out, 0, sizeof(int64_t), st);
+    return run_scan<SumI64, false, false>(in, out, n, tmp, tmp_bytes, st);
+}
+
+cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
+                               cudaStream_t st)
+{
+    if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
+    return run_scan<SumU64, false, false>(in, out, n, tmp, tmp_bytes, st);
+}
+
+cudaError_t suffix_max_f64(const double *in, double *out, int64_t n, void *tmp, size_t tmp_bytes,
+                           cudaStream_t st)
+{
+    k_set_f64<<<1, 1, 0, st>>>(out + n, 0.0);
+    return run_scan<MaxF64, true, true>(in, out, n, tmp, tmp_bytes, st);
+}
+
+}  // namespace fm

@@ -1,0 +1,255 @@
+"""Python binding of the C-ABI in include/fastmaxent.h (ctypes; argument marshalling only).
+
+Every step of the sampler runs in libfastmaxent.so's sm_100a kernels.  There is no CPU fallback:
+importing this module raises if the library is missing, and every call raises FastMaxEntError
+on a non-OK status (e.g. FM_ERR_CUDA when no device is present).
+
+    plan  = sort_plan(x, y=None, seg_target=256)         # fm_sort_plan   (a1-a4)
+    edges = sample_ubcm(plan, seed, n_samples)           # fm_sample_ubcm (a5-a6)
+    edges = sample_ecm(plan, seed, n_samples)            # fm_sample_ecm
+    edges.edges   -> torch.int32 [E, 2] on the GPU (zero-copy), edges.weights -> [E] (ECM)
+    edges.offsets -> numpy int64 [n_samples + 1]
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfastmaxent.so")
+
+FM_UBCM, FM_ECM = 0, 1
+FM_OK, FM_ERR_INVALID, FM_ERR_NOMEM, FM_ERR_CUDA, FM_ERR_BOUND, FM_ERR_STATE = 0, -1, -2, -3, -4, -5
+FM_FLAG_WEIGHT_SATURATED, FM_FLAG_SCRATCH_RERUN = 1, 2
+STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ERR_CUDA", -4: "FM_ERR_BOUND",
+                -5: "FM_ERR_STATE"}
+SYMBOLS = ["fm_sort_plan", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
+           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version"]
+
+
+class FastMaxEntError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Edges(C.Structure):
+    _fields_ = [("n_samples", C.c_int64), ("n_edges", C.c_int64), ("offsets", C.POINTER(C.c_int64)),
+                ("edges", C.c_void_p), ("weights", C.c_void_p), ("draws", C.c_int64), ("landed", C.c_int64),
+                ("accepted", C.c_int64), ("segments", C.c_int64), ("chunks", C.c_int64), ("flags", C.c_uint32),
+                ("_owner", C.c_void_p)]
+
+
+class _PlanInfo(C.Structure):
+    _fields_ = [("model", C.c_int32), ("n", C.c_int64), ("seg_target", C.c_int64), ("F", C.c_int32),
+                ("n_segments", C.c_int64), ("n_chunks", C.c_int64), ("est_draws", C.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"{LIB_PATH} is missing: build it with `python -m paper_2509_13230_b200.build` "
+                      "(nvcc, sm_100a). There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, u64 = C.c_void_p, C.c_int64, C.c_uint64
+    L.fm_sort_plan.argtypes = [C.c_int, i64, vp, vp, i64, vp, C.POINTER(vp)]
+    L.fm_sort_plan.restype = C.c_int
+    for f in (L.fm_sample_ubcm, L.fm_sample_ecm):
+        f.argtypes = [vp, u64, i64, i64, vp, C.POINTER(_Edges)]
+        f.restype = C.c_int
+    L.fm_edges_to_host.argtypes = [C.POINTER(_Edges), vp, vp, vp]
+    L.fm_edges_to_host.restype = C.c_int
+    L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
+    L.fm_plan_get_info.restype = C.c_int
+    L.fm_plan_export.argtypes = [vp] + [vp] * 8
+    L.fm_plan_export.restype = C.c_int
+    L.fm_free.argtypes = [vp]
+    L.fm_free.restype = None
+    L.fm_last_error.argtypes = []
+    L.fm_last_error.restype = C.c_char_p
+    L.fm_abi_version.argtypes = []
+    L.fm_abi_version.restype = C.c_int32
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != FM_OK:
+        raise FastMaxEntError(status, lib.fm_last_error().decode(errors="replace"))
+
+
+def _stream(stream):
+    if stream is not None:
+        return C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    except ImportError:  # pragma: no cover
+        pass
+    return C.c_void_p(0)
+
+
+def _as_f64(a):
+    """(pointer, keepalive) for a float64 vector: torch tensor (CUDA or CPU) or array-like (host)."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64:
+                a = a.to(torch.float64)
+            a = a.contiguous()
+            return C.c_void_p(a.data_ptr()), a, a.numel()
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return C.c_void_p(arr.ctypes.data), arr, arr.size
+
+
+class _CAI:
+    """__cuda_array_interface__ view of library-owned device memory; keeps its owner alive."""
+
+    def __init__(self, ptr, shape, typestr, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3, "strides": None}
+
+
+class Plan:
+    def __init__(self, handle, model):
+        self._h = handle
+        self.model = model
+        info = _PlanInfo()
+        _check(lib.fm_plan_get_info(self._h, C.byref(info)))
+        self.n = info.n
+        self.seg_target = info.seg_target
+        self.F = info.F
+        self.n_segments = info.n_segments
+        self.n_chunks = info.n_chunks
+        self.est_draws = info.est_draws
+
+    def export(self) -> dict:
+        n, s = self.n, self.n_segments
+        ecm = self.model == FM_ECM
+        out = {"perm": np.empty(n, np.int32), "kappa_s": np.empty(n, np.float64),
+               "y_s": np.empty(n, np.float64) if ecm else None, "ymax": np.empty(n + 1, np.float64) if ecm else None,
+               "seg": np.empty((s, 4), np.int32), "seg_h0": np.empty(s), "seg_q0": np.empty(s),
+               "seg_omT": np.empty(s)}
+        ptr = lambda a: None if a is None else C.c_void_p(a.ctypes.data)  # noqa: E731
+        _check(lib.fm_plan_export(self._h, *(ptr(out[k]) for k in ("perm", "kappa_s", "y_s", "ymax", "seg", "seg_h0",
+                                                                    "seg_q0", "seg_omT"))))
+        return out
+
+    def free(self):
+        if self._h:
+            lib.fm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # pragma: no cover
+            pass
+
+
+class Edges:
+    """Result of fm_sample_*: device edge list (+ weights), host offsets, counters."""
+
+    def __init__(self, st: _Edges, stream):
+        self._st = st
+        self._stream = stream
+        self.n_samples = st.n_samples
+        self.n_edges = st.n_edges
+        self.offsets = np.ctypeslib.as_array(st.offsets, shape=(st.n_samples + 1,)).copy() if st.offsets else \
+            np.zeros(1, np.int64)
+        self.draws, self.landed, self.accepted = st.draws, st.landed, st.accepted
+        self.segments, self.chunks, self.flags = st.segments, st.chunks, st.flags
+        self._edges_t = None
+        self._w_t = None
+
+    @property
+    def edges(self):
+        """torch.int32 [n_edges, 2] on the GPU (zero-copy view of library memory)."""
+        if self._edges_t is None:
+            import torch
+            self._edges_t = torch.as_tensor(_CAI(self._st.edges, (self.n_edges, 2), "<i4", self), device="cuda")
+        return self._edges_t
+
+    @property
+    def weights(self):
+        if not self._st.weights:
+            return None
+        if self._w_t is None:
+            import torch
+            self._w_t = torch.as_tensor(_CAI(self._st.weights, (self.n_edges,), "<i4", self), device="cuda")
+        return self._w_t
+
+    def to_host(self, edges_out=None, weights_out=None, stream=None):
+        """fm_edges_to_host into (optionally caller-provided, e.g. pinned) host buffers -> numpy."""
+        if edges_out is None:
+            edges_out = np.empty((self.n_edges, 2), np.int32)
+        has_w = bool(self._st.weights)
+        if has_w and weights_out is None:
+            weights_out = np.empty(self.n_edges, np.int32)
+        ep = edges_out.data_ptr() if hasattr(edges_out, "data_ptr") else edges_out.ctypes.data
+        wp = None
+        if has_w:
+            wp = weights_out.data_ptr() if hasattr(weights_out, "data_ptr") else weights_out.ctypes.data
+        _check(lib.fm_edges_to_host(C.byref(self._st), C.c_void_p(ep), C.c_void_p(wp) if wp else None,
+                                    _stream(stream) if stream is not None else self._stream))
+        return edges_out, (weights_out if has_w else None)
+
+    def sample(self, s: int):
+        a, b = int(self.offsets[s]), int(self.offsets[s + 1])
+        return self.edges[a:b], (None if self.weights is None else self.weights[a:b])
+
+    def free(self):
+        if self._st is not None and self._st._owner:
+            self._edges_t = None
+            self._w_t = None
+            lib.fm_free(C.byref(self._st))
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # pragma: no cover
+            pass
+
+
+def sort_plan(x, y=None, seg_target: int = 256, stream=None) -> Plan:
+    """fm_sort_plan: validate, sort (descending kappa), beta_min suffix max, segment plan."""
+    model = FM_UBCM if y is None else FM_ECM
+    xp, xk, n = _as_f64(x)
+    yp = None
+    yk = None
+    if y is not None:
+        yp, yk, ny = _as_f64(y)
+        if ny != n:
+            raise FastMaxEntError(FM_ERR_INVALID, f"len(y) = {ny} != len(x) = {n}")
+    h = C.c_void_p()
+    _check(lib.fm_sort_plan(model, n, xp, yp, int(seg_target), _stream(stream), C.byref(h)))
+    del xk, yk
+    return Plan(h, model)
+
+
+def _sample(fn, plan: Plan, seed: int, n_samples: int, first_sample: int, stream) -> Edges:
+    st = _Edges()
+    s = _stream(stream)
+    _check(fn(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples), s, C.byref(st)))
+    return Edges(st, s)
+
+
+def sample_ubcm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None) -> Edges:
+    """fm_sample_ubcm."""
+    return _sample(lib.fm_sample_ubcm, plan, seed, n_samples, first_sample, stream)
+
+
+def sample_ecm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None) -> Edges:
+    """fm_sample_ecm (Algorithm 1)."""
+    return _sample(lib.fm_sample_ecm, plan, seed, n_samples, first_sample, stream)
+
+
+def abi_version() -> int:
+    return int(lib.fm_abi_version())
