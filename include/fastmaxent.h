@@ -118,6 +118,20 @@ fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info);
 fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax,
                          int32_t *seg, double *seg_h0, double *seg_q0, double *seg_omT);
 
+/* Device-side phase timing (for benchmarks).  When enabled, CUDA events are recorded on the
+ * call's stream around each phase; fm_timing_get synchronises those events and returns the
+ * accumulated milliseconds since the last reset.  `launches` counts every kernel the library
+ * launched (whether or not timing is enabled). */
+typedef struct {
+    double plan_ms;     /* fm_sort_plan, all a1-a4 kernels                                  */
+    double sample_ms;   /* the sampler kernel(s) k_sample (a5)                              */
+    double write_ms;    /* count scan + compaction (a6), incl. overflow re-runs             */
+    int64_t sample_launches;
+    int64_t launches;
+} fm_timing;
+fm_status fm_timing_enable(int on);
+fm_status fm_timing_get(fm_timing *t, int reset);
+
 /* Release an fm_plan* or the buffers of an fm_edges* (the struct itself is caller-owned and
  * is zeroed).  Objects are tagged; NULL is a no-op. */
 void fm_free(void *obj);

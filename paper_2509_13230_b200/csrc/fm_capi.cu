@@ -1,6 +1,7 @@
 // fm_capi.cu -- the C-ABI (include/fastmaxent.h): validation, stream-ordered memory, launch
 // orchestration of the a1-a6 kernels, status codes.
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -13,9 +14,47 @@
 #include "fm_internal.cuh"
 #include "fm_plan_kernels.cuh"
 
+namespace fm {
+std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+}  // namespace fm
+
 using namespace fm;
 
 namespace {
+
+// ---- optional device-side phase timing (fm_timing_*) ----
+enum { kPhasePlan = 0, kPhaseSample = 1, kPhaseWrite = 2 };
+struct Pending {
+    int phase;
+    cudaEvent_t a, b;
+};
+std::mutex g_tmu;
+std::vector<Pending> g_pending;
+std::atomic<bool> g_timing{false};
+double g_phase_ms[3] = {0, 0, 0};
+long long g_sample_launches = 0;
+
+struct PhaseTimer {
+    int phase = -1;
+    cudaEvent_t a = nullptr, b = nullptr;
+    void begin(int ph, cudaStream_t st)
+    {
+        if (!g_timing.load()) return;
+        phase = ph;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+    }
+    void end(cudaStream_t st)
+    {
+        if (phase < 0) return;
+        cudaEventRecord(b, st);
+        std::lock_guard<std::mutex> lk(g_tmu);
+        g_pending.push_back({phase, a, b});
+        phase = -1;
+    }
+};
 
 thread_local std::string g_err;
 std::mutex g_mu;
@@ -160,6 +199,8 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(cudaGetDevice(&dev), "cudaGetDevice");
     configure_pool_once(dev);
     Allocs tmp(st);
+    PhaseTimer timer;
+    timer.begin(kPhasePlan, st);
 
     // ---- inputs: host or device ----
     const double *xd = x, *yd = y;
@@ -189,6 +230,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     memset(&h_sc, 0, sizeof(h_sc));
     h_sc.key_and = ~0ull;
     CK(cudaMemcpyAsync(sc, &h_sc, sizeof(h_sc), cudaMemcpyHostToDevice, st), "init scalars");
+    count_launch();
     k_validate_key<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, xd, yd, ka, ia, sc);
     CK(cudaGetLastError(), "k_validate_key");
     CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
@@ -224,6 +266,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
         CK(cudaMallocAsync((void **)&p->y_s, sizeof(double) * n, st), "alloc y_s");
         CK(cudaMallocAsync((void **)&p->ymax, sizeof(double) * (n + 1), st), "alloc ymax");
     }
+    count_launch();
     k_gather_sorted<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, skeys, yd, p->perm, p->kappa_s, p->y_s);
     CK(cudaGetLastError(), "k_gather_sorted");
 
@@ -237,10 +280,13 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(tmp.get(&P, n + 1), "alloc P");
     CK(tmp.get(&rows, n), "alloc rows");
     CK(tmp.get(&row_m, n + 1), "alloc row_m");
+    count_launch();
     k_set_F<<<1, 1, 0, st>>>(n, ceil_log2(n), p->kappa_s, sc);
+    count_launch();
     k_kfx<<<grid_for(n, 256), 256, 0, st>>>(n, p->kappa_s, sc, P);
     CK(cudaGetLastError(), "k_kfx");
     CK(scan_exclusive_u64(P, P, n, work, tmp_bytes, st), "scan P");
+    count_launch();
     k_rows<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, seg_target, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
                                              row_m);
     CK(cudaGetLastError(), "k_rows");
@@ -260,6 +306,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(cudaMallocAsync((void **)&p->seg_omT, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_omT");
     int64_t *seg_work;
     CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
+    count_launch();
     k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n, n_seg, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
                                                  row_m, p->seg, p->seg_h0, p->seg_q0, p->seg_omT, seg_work);
     CK(cudaGetLastError(), "k_emit");
@@ -277,6 +324,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     p->chunk_target = target;
     p->n_chunks = std::max<int64_t>(1, (total + target - 1) / target);
     CK(cudaMallocAsync((void **)&p->chunk_seg, sizeof(int64_t) * (p->n_chunks + 1), st), "alloc chunks");
+    count_launch();
     k_chunks<<<grid_for(p->n_chunks + 1, 256), 256, 0, st>>>(n_seg, p->n_chunks, target, seg_work, p->chunk_seg);
     CK(cudaGetLastError(), "k_chunks");
     // scratch slot per task: chunk work < target + wmax (DESIGN 7.2); edges <= draws
@@ -286,6 +334,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     if (cap_override > 0) p->cap = cap_override;
 
     CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
+    timer.end(st);
     CK(cudaStreamSynchronize(st), "sync (plan)");
     if (h_sc.flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
 
@@ -382,7 +431,15 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.counts = counts;
         a.counters = hd->counters;
         a.flags = &hd->flags;
+        PhaseTimer ts, tw;
+        ts.begin(kPhaseSample, st);
         CK(launch_sample(model, a, st), "sampler launch");
+        ts.end(st);
+        tw.begin(kPhaseWrite, st);
+        if (g_timing.load()) {
+            std::lock_guard<std::mutex> lk(g_tmu);
+            g_sample_launches++;
+        }
         CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
         CK(launch_offsets(n_samples, p->n_chunks, dest, offs_d, st), "offsets");
         CK(launch_overflow(n_tasks, p->cap, counts, &hd->n_overflow, ovl, st), "overflow check");
@@ -405,6 +462,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             r.weights = (int32_t *)own->weights;
             CK(launch_sample(model, r, st), "rerun launch");
         }
+        tw.end(st);
         out->n_edges = total;
     }
     out->n_samples = n_samples;
@@ -490,6 +548,36 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->seg_h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
     if (seg_q0 && s) CK(cudaMemcpy(seg_q0, p->seg_q0, s * 8, cudaMemcpyDeviceToHost), "seg_q0");
     if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->seg_omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
+    return FM_OK;
+}
+
+fm_status fm_timing_enable(int on)
+{
+    g_timing.store(on != 0);
+    return FM_OK;
+}
+
+fm_status fm_timing_get(fm_timing *t, int reset)
+{
+    if (!t) return fail(FM_ERR_INVALID, "NULL timing");
+    std::lock_guard<std::mutex> lk(g_tmu);
+    for (auto &pd : g_pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(pd.b) == cudaSuccess && cudaEventElapsedTime(&ms, pd.a, pd.b) == cudaSuccess)
+            g_phase_ms[pd.phase] += ms;
+        cudaEventDestroy(pd.a);
+        cudaEventDestroy(pd.b);
+    }
+    g_pending.clear();
+    t->plan_ms = g_phase_ms[kPhasePlan];
+    t->sample_ms = g_phase_ms[kPhaseSample];
+    t->write_ms = g_phase_ms[kPhaseWrite];
+    t->sample_launches = g_sample_launches;
+    t->launches = g_launches.load();
+    if (reset) {
+        g_phase_ms[0] = g_phase_ms[1] = g_phase_ms[2] = 0;
+        g_sample_launches = 0;
+    }
     return FM_OK;
 }
 

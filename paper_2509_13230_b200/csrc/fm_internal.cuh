@@ -77,6 +77,9 @@ __device__ __forceinline__ double u01(uint32_t k)
     return __dmul_rn(__dadd_rn((double)k, 0.5), 0x1p-32);
 }
 
+// every kernel launch of the library is counted (fm_timing.launches)
+void count_launch(int n = 1);
+
 // ------------------------------------------------------------------------------------------
 // launch helpers (fm_scan.cu)
 // ------------------------------------------------------------------------------------------

@@ -199,6 +199,7 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
 {
     if (a.n_tasks <= 0) return cudaSuccess;
     const int64_t blocks = (a.n_tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    count_launch();
     if (model == FM_UBCM)
         k_sample<FM_UBCM><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, st>>>(a);
     else
@@ -210,6 +211,7 @@ cudaError_t launch_overflow(int64_t n_tasks, int64_t cap, const int64_t *counts,
                             int64_t *overflow_list, cudaStream_t st)
 {
     if (n_tasks <= 0) return cudaSuccess;
+    count_launch();
     k_overflow<<<(unsigned)((n_tasks + 255) / 256), 256, 0, st>>>(n_tasks, cap, counts, n_overflow, overflow_list);
     return cudaGetLastError();
 }
@@ -220,12 +222,14 @@ cudaError_t launch_compact(int64_t n_tasks, int64_t cap, const int64_t *counts, 
 {
     if (n_tasks <= 0) return cudaSuccess;
     const int64_t grid = n_tasks < 1048576 ? n_tasks : 1048576;
+    count_launch();
     k_compact<<<(unsigned)grid, 256, 0, st>>>(n_tasks, cap, counts, dest, scratch_e, scratch_w, out_e, out_w);
     return cudaGetLastError();
 }
 
 cudaError_t launch_offsets(int64_t n_samples, int64_t n_chunks, const int64_t *dest, int64_t *offsets, cudaStream_t st)
 {
+    count_launch();
     k_offsets<<<(unsigned)((n_samples + 1 + 255) / 256), 256, 0, st>>>(n_samples, n_chunks, dest, offsets);
     return cudaGetLastError();
 }

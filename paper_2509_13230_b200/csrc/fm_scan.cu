@@ -138,8 +138,11 @@ cudaError_t run_scan(const typename Op::T *in, typename Op::T *out, int64_t n, v
     const int64_t nb = (n + kTile - 1) / kTile;
     if (tmp_bytes < sizeof(T) * (size_t)nb) return cudaErrorInvalidValue;
     T *partial = (T *)tmp;
+    count_launch();
     k_tile_reduce<Op, kRev><<<(unsigned)nb, kThreads, 0, st>>>(in, n, partial);
+    count_launch();
     k_partials<Op><<<1, kThreads, 0, st>>>(partial, nb);
+    count_launch();
     k_tile_scan<Op, kRev, kInclusive><<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, partial, nb);
     return cudaGetLastError();
 }
@@ -167,6 +170,7 @@ cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, voi
 cudaError_t suffix_max_f64(const double *in, double *out, int64_t n, void *tmp, size_t tmp_bytes,
                            cudaStream_t st)
 {
+    count_launch();
     k_set_f64<<<1, 1, 0, st>>>(out + n, 0.0);
     return run_scan<MaxF64, true, true>(in, out, n, tmp, tmp_bytes, st);
 }

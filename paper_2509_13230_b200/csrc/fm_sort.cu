@@ -105,9 +105,11 @@ cudaError_t radix_sort_u64_i32(uint64_t *keys_a, uint64_t *keys_b, int32_t *vals
     int32_t *vi = vals_a, *vo = vals_b;
     for (int shift = 0; shift < 64; shift += 8) {
         if (((vary_bits >> shift) & 0xFFull) == 0) continue;
+        count_launch();
         k_hist<<<(unsigned)nt, kThreads, 0, st>>>(ki, n, shift, nt, counts);
         cudaError_t e = scan_exclusive_i64(counts, counts, m, scan_tmp, scan_tmp_bytes(m), st);
         if (e != cudaSuccess) return e;
+        count_launch();
         k_scatter<<<(unsigned)nt, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, nt, counts);
         uint64_t *tk = ki; ki = ko; ko = tk;
         int32_t *tv = vi; vi = vo; vo = tv;

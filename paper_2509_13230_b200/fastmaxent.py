@@ -26,7 +26,7 @@ FM_FLAG_WEIGHT_SATURATED, FM_FLAG_SCRATCH_RERUN = 1, 2
 STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ERR_CUDA", -4: "FM_ERR_BOUND",
                 -5: "FM_ERR_STATE"}
 SYMBOLS = ["fm_sort_plan", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
-           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version"]
+           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get"]
 
 
 class FastMaxEntError(RuntimeError):
@@ -45,6 +45,11 @@ class _Edges(C.Structure):
 class _PlanInfo(C.Structure):
     _fields_ = [("model", C.c_int32), ("n", C.c_int64), ("seg_target", C.c_int64), ("F", C.c_int32),
                 ("n_segments", C.c_int64), ("n_chunks", C.c_int64), ("est_draws", C.c_int64)]
+
+
+class _Timing(C.Structure):
+    _fields_ = [("plan_ms", C.c_double), ("sample_ms", C.c_double), ("write_ms", C.c_double),
+                ("sample_launches", C.c_int64), ("launches", C.c_int64)]
 
 
 def _load():
@@ -70,6 +75,10 @@ def _load():
     L.fm_last_error.restype = C.c_char_p
     L.fm_abi_version.argtypes = []
     L.fm_abi_version.restype = C.c_int32
+    L.fm_timing_enable.argtypes = [C.c_int]
+    L.fm_timing_enable.restype = C.c_int
+    L.fm_timing_get.argtypes = [C.POINTER(_Timing), C.c_int]
+    L.fm_timing_get.restype = C.c_int
     return L
 
 
@@ -253,3 +262,16 @@ def sample_ecm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0,
 
 def abi_version() -> int:
     return int(lib.fm_abi_version())
+
+
+def timing_enable(on: bool = True) -> None:
+    """Record CUDA events around each library phase (fm_timing_enable)."""
+    _check(lib.fm_timing_enable(1 if on else 0))
+
+
+def timing_get(reset: bool = False) -> dict:
+    """Accumulated device milliseconds per phase and the library's kernel-launch count."""
+    t = _Timing()
+    _check(lib.fm_timing_get(C.byref(t), 1 if reset else 0))
+    return {"plan_ms": t.plan_ms, "sample_ms": t.sample_ms, "write_ms": t.write_ms,
+            "sample_launches": t.sample_launches, "launches": t.launches}
