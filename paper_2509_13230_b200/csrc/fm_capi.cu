@@ -156,7 +156,9 @@ void plan_release(Plan *p)
     cudaFree(p->seg_h0);
     cudaFree(p->seg_q0);
     cudaFree(p->seg_omT);
+    cudaFree(p->rec);
     cudaFree(p->chunk_seg);
+    cudaFree(p->chunk_cap);
     p->magic = 0;
     delete p;
 }
@@ -310,6 +312,11 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n, n_seg, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
                                                  row_m, p->seg, p->seg_h0, p->seg_q0, p->seg_omT, seg_work);
     CK(cudaGetLastError(), "k_emit");
+    CK(cudaMallocAsync((void **)&p->rec, sizeof(SegRec) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
+    count_launch();
+    k_pack<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n_seg, p->seg, p->seg_h0, p->seg_q0, p->seg_omT,
+                                                 p->kappa_s, p->perm, p->y_s, p->rec);
+    CK(cudaGetLastError(), "k_pack");
     {
         const size_t wb = scan_tmp_bytes(n_seg + 1);
         char *work2;
@@ -317,21 +324,33 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
         CK(scan_exclusive_i64(seg_work, seg_work, n_seg, work2, wb, st), "scan work");
     }
 
-    // ---- chunking (never changes results) ----
-    const int64_t lane_draws = std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 256));
-    const int64_t target = 32 * lane_draws * kUnit;
+    // ---- lane-chunking (never changes results) ----
+    const int64_t lane_draws = std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128));
+    const int64_t target = lane_draws * kUnit;
     const int64_t total = h_sc.total_work;
     p->chunk_target = target;
     p->n_chunks = std::max<int64_t>(1, (total + target - 1) / target);
     CK(cudaMallocAsync((void **)&p->chunk_seg, sizeof(int64_t) * (p->n_chunks + 1), st), "alloc chunks");
+    CK(cudaMallocAsync((void **)&p->chunk_cap, sizeof(int64_t) * (p->n_chunks + 1), st), "alloc chunk caps");
     count_launch();
-    k_chunks<<<grid_for(p->n_chunks + 1, 256), 256, 0, st>>>(n_seg, p->n_chunks, target, seg_work, p->chunk_seg);
+    k_chunks<<<grid_for(p->n_chunks, 256), 256, 0, st>>>(n_seg, p->n_chunks, target, seg_work, p->chunk_seg,
+                                                          p->chunk_cap);
     CK(cudaGetLastError(), "k_chunks");
-    // scratch slot per task: chunk work < target + wmax (DESIGN 7.2); edges <= draws
-    const double est = (double)(target + p->wmax) / (double)kUnit;
-    p->cap = (int64_t)(est * 1.25) + 256;
+    {
+        const size_t cb = scan_tmp_bytes(p->n_chunks + 1);
+        char *work3;
+        CK(tmp.get(&work3, cb), "alloc scan tmp");
+        CK(scan_exclusive_i64(p->chunk_cap, p->chunk_cap, p->n_chunks, work3, cb, st), "scan chunk caps");
+    }
+    // sum over chunks of floor(1.25 w_c / 2^G) + 16 <= floor(1.25 total / 2^G) + 16 n_chunks
+    p->cap_per_sample = ((total + total / 4) >> kG) + 16 * p->n_chunks + 16;
     const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
-    if (cap_override > 0) p->cap = cap_override;
+    if (cap_override > 0) {
+        count_launch();
+        k_fill_caps<<<grid_for(p->n_chunks + 1, 256), 256, 0, st>>>(p->chunk_cap, p->n_chunks, cap_override);
+        CK(cudaGetLastError(), "k_fill_caps");
+        p->cap_per_sample = cap_override * p->n_chunks;
+    }
 
     CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
     timer.end(st);
@@ -389,17 +408,21 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         unsigned int flags;
         unsigned int pad;
         unsigned long long n_overflow;
+        unsigned long long task_counter;
+        unsigned long long spill_counter;
     };
     Hdr h;
     memset(&h, 0, sizeof(h));
     if (n_tasks > 0) {
         int2 *se;
         int32_t *sw = nullptr;
-        int64_t *counts, *dest, *ovl, *offs_d;
+        int64_t *counts, *dest, *ovl, *offs_d, *spill_off;
         Hdr *hd;
-        const int64_t slots = n_tasks * p->cap;
-        CK(tmp.get(&se, slots), "alloc scratch edges");
-        if (model == FM_ECM) CK(tmp.get(&sw, slots), "alloc scratch weights");
+        const int64_t slots = n_samples * p->cap_per_sample;
+        const int64_t spill_cap = slots / 32 + 65536;
+        CK(tmp.get(&se, slots + spill_cap), "alloc scratch edges");
+        if (model == FM_ECM) CK(tmp.get(&sw, slots + spill_cap), "alloc scratch weights");
+        CK(tmp.get(&spill_off, n_tasks), "alloc spill offsets");
         CK(tmp.get(&counts, n_tasks + 1), "alloc counts");
         CK(tmp.get(&dest, n_tasks + 1), "alloc dest");
         CK(tmp.get(&ovl, n_tasks), "alloc overflow list");
@@ -412,23 +435,26 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
 
         SampleArgs a;
         memset(&a, 0, sizeof(a));
-        a.seg = p->seg;
-        a.seg_h0 = p->seg_h0;
-        a.seg_q0 = p->seg_q0;
-        a.seg_omT = p->seg_omT;
+        a.rec = p->rec;
         a.kappa_s = p->kappa_s;
         a.y_s = p->y_s;
         a.perm = p->perm;
         a.chunk_seg = p->chunk_seg;
+        a.chunk_cap = p->chunk_cap;
         a.n_chunks = p->n_chunks;
-        a.cap = p->cap;
-        a.k0 = (uint32_t)(seed & 0xffffffffu);
-        a.k1 = (uint32_t)(seed >> 32);
+        a.cap_per_sample = p->cap_per_sample;
+        a.key = philox_key(seed);
         a.first_sample = (uint32_t)first_sample;
         a.n_tasks = n_tasks;
+        a.task_counter = &hd->task_counter;
         a.edges = se;
         a.weights = sw;
         a.counts = counts;
+        a.spill_e = se + slots;
+        a.spill_w = sw ? sw + slots : nullptr;
+        a.spill_counter = &hd->spill_counter;
+        a.spill_cap = spill_cap;
+        a.spill_off = spill_off;
         a.counters = hd->counters;
         a.flags = &hd->flags;
         PhaseTimer ts, tw;
@@ -442,7 +468,8 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         }
         CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
         CK(launch_offsets(n_samples, p->n_chunks, dest, offs_d, st), "offsets");
-        CK(launch_overflow(n_tasks, p->cap, counts, &hd->n_overflow, ovl, st), "overflow check");
+        CK(launch_overflow(n_tasks, p->n_chunks, p->chunk_cap, counts, spill_off, &hd->n_overflow, ovl, st),
+           "overflow check");
         CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
            "read offsets");
         CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
@@ -451,9 +478,10 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         CK(cudaMallocAsync(&own->edges, sizeof(int2) * std::max<int64_t>(total, 1), st), "alloc edges");
         if (model == FM_ECM)
             CK(cudaMallocAsync(&own->weights, sizeof(int32_t) * std::max<int64_t>(total, 1), st), "alloc weights");
-        CK(launch_compact(n_tasks, p->cap, counts, dest, se, sw, (int2 *)own->edges, (int32_t *)own->weights, st),
+        CK(launch_compact(total, n_tasks, p->n_chunks, p->cap_per_sample, p->chunk_cap, counts, dest, spill_off, se, sw,
+                          a.spill_e, a.spill_w, (int2 *)own->edges, (int32_t *)own->weights, st),
            "compact");
-        if (h.n_overflow) {  // deterministic re-run of overflowed chunks straight into the final array
+        if (h.n_overflow) {  // deterministic re-run of overflowed tasks straight into the final array
             SampleArgs r = a;
             r.n_tasks = (int64_t)h.n_overflow;
             r.task_list = ovl;
@@ -548,6 +576,13 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->seg_h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
     if (seg_q0 && s) CK(cudaMemcpy(seg_q0, p->seg_q0, s * 8, cudaMemcpyDeviceToHost), "seg_q0");
     if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->seg_omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
+    return FM_OK;
+}
+
+fm_status fm_debug_eval(int32_t fn, int64_t n, const double *in_dev, double *out_dev, void *cuda_stream)
+{
+    if (fn < 0 || fn > 2 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return fail(FM_ERR_INVALID, "bad debug_eval args");
+    CK(launch_debug_eval(fn, n, in_dev, out_dev, (cudaStream_t)cuda_stream), "debug eval");
     return FM_OK;
 }
 

@@ -21,6 +21,15 @@ enum : uint32_t {
     kFlagWeightSat = 8u,  // ECM weight clamped
 };
 
+// one plan segment as the sampler reads it (64 B, two halves of 32 B; UBCM reads the first 48 B)
+struct __align__(16) SegRec {
+    int32_t u, a, b, sigma;  // focal rank, candidates [a, b), segment index in the row
+    double h0, q0;           // initial bound at a-1: h0 = -log(1 - q0), q0
+    double ku;               // kappa_s[u]
+    int32_t id_u, pad;       // perm[u]
+    double yu, omT;          // ECM: y_s[u], 1 - T
+};
+
 struct Plan {
     uint32_t magic;
     int model;
@@ -38,13 +47,15 @@ struct Plan {
     double *seg_h0;     // [n_seg]
     double *seg_q0;     // [n_seg]
     double *seg_omT;    // [n_seg] ECM (1.0 for UBCM)
+    SegRec *rec;        // [n_seg] packed copy of the above for the sampler
     int64_t est_draws;  // sum of segment work estimates / 2^G
     // chunking (does not change results)
     int64_t n_chunks;
-    int64_t *chunk_seg;   // [n_chunks+1] first segment of each chunk
-    int64_t chunk_target; // work per chunk (units 2^G)
+    int64_t *chunk_seg;   // [n_chunks+1] first segment of each lane-chunk
+    int64_t *chunk_cap;   // [n_chunks+1] exclusive prefix of the lane-chunk scratch slots (edges)
+    int64_t chunk_target; // work per lane-chunk (units 2^G)
     int64_t wmax;         // bound of one segment's work (units 2^G)
-    int64_t cap;          // scratch slot per (sample, chunk), edges
+    int64_t cap_per_sample;  // scratch edges per sample (upper bound of chunk_cap[n_chunks])
 };
 
 struct Owner {
@@ -58,6 +69,34 @@ struct Owner {
 // ------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11) -- DESIGN.md R1.
 // ------------------------------------------------------------------------------------------
+// round keys k + r * (0x9E3779B9, 0xBB67AE85), r = 0..9 (precomputed on the host: the kernel
+// reads them from the constant bank as LOP3 operands)
+struct PhiloxKey {
+    uint32_t k0[10], k1[10];
+};
+inline PhiloxKey philox_key(uint64_t seed)
+{
+    PhiloxKey K;
+    uint32_t a = (uint32_t)(seed & 0xffffffffu), b = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; r++) {
+        K.k0[r] = a;
+        K.k1[r] = b;
+        a += 0x9E3779B9u;
+        b += 0xBB67AE85u;
+    }
+    return K;
+}
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxKey &K)
+{
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ K.k0[r], lo1, hi0 ^ c.w ^ K.k1[r], lo0);
+    }
+    return c;
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
 {
 #pragma unroll

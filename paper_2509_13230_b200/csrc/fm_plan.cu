@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) k_rows(int model, int64_t n, int64_t S, c
                                               int64_t *__restrict__ row_m)
 {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    long long work = 0;
+    long long work = 0, wseg = 0;
     if (u < n - 1) {
         const int F = sc->F;
         double r = kappa_s[u];
@@ -111,15 +111,20 @@ __global__ void __launch_bounds__(256) k_rows(int model, int64_t n, int64_t S, c
         row_m[u] = m;
         work = WN + m * kUnit;
         // bound of one segment's work: Wtot (unsplit) or ceil(Wtot/m) + 2 units + 2 (DESIGN 7.2)
-        const int64_t wseg = m == 1 ? Wt : (Wt + m - 1) / m + 2 * kUnit + 2;
-        atomicMax(&sc->wmax, (long long)wseg);
+        wseg = m == 1 ? Wt : (Wt + m - 1) / m + 2 * kUnit + 2;
     } else if (u == n - 1) {
         row_m[u] = 0;
     }
     // block reduce of work (int64)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
-    if ((threadIdx.x & 31) == 0 && work) atomicAdd((unsigned long long *)&sc->total_work, (unsigned long long)work);
+    for (int o = 16; o > 0; o >>= 1) {
+        work += __shfl_xor_sync(0xffffffffu, work, o);
+        wseg = max(wseg, __shfl_xor_sync(0xffffffffu, wseg, o));
+    }
+    if ((threadIdx.x & 31) == 0 && work) {
+        atomicAdd((unsigned long long *)&sc->total_work, (unsigned long long)work);
+        atomicMax(&sc->wmax, wseg);
+    }
 }
 
 // cut k of row u (1 <= k < m): smallest v in [u+2, n-1] with W_u(v) >= floor(k Wtot / m), n-1 if none
@@ -181,23 +186,61 @@ __global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_se
     seg_work[g] = wb - wa + kUnit;
 }
 
-// chunking: chunk c starts at the first segment whose work prefix reaches c * target
+// chunking: lane-chunk c starts at the first segment whose work prefix reaches c * target;
+// its scratch slot holds floor(1.25 * est_draws) + 16 edges (edges <= draws)
 __global__ void __launch_bounds__(256) k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target,
-                                                const int64_t *__restrict__ work_pre, int64_t *__restrict__ chunk_seg)
+                                                const int64_t *__restrict__ work_pre, int64_t *__restrict__ chunk_seg,
+                                                int64_t *__restrict__ chunk_cap)
 {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c > n_chunks) return;
-    if (c == n_chunks) {
-        chunk_seg[c] = n_seg;
-        return;
-    }
-    const int64_t th = c * target;
-    int64_t lo = 0, hi = n_seg;  // smallest g with work_pre[g] >= th
-    while (lo < hi) {
-        const int64_t mid = lo + ((hi - lo) >> 1);
-        if (work_pre[mid] >= th) hi = mid; else lo = mid + 1;
-    }
-    chunk_seg[c] = lo;
+    if (c >= n_chunks) return;
+    auto start = [&](int64_t cc) -> int64_t {
+        if (cc >= n_chunks) return n_seg;
+        const int64_t th = cc * target;
+        int64_t lo = 0, hi = n_seg;  // smallest g with work_pre[g] >= th
+        while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if (work_pre[mid] >= th) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    const int64_t g0 = start(c), g1 = start(c + 1);
+    chunk_seg[c] = g0;
+    if (c == n_chunks - 1) chunk_seg[n_chunks] = n_seg;
+    const int64_t w = work_pre[g1] - work_pre[g0];
+    chunk_cap[c] = ((w + (w >> 2)) >> kG) + 16;
+}
+
+// packed per-segment records for the sampler (one 64-byte load instead of five gathers)
+__global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, const int4 *__restrict__ seg,
+                                              const double *__restrict__ seg_h0, const double *__restrict__ seg_q0,
+                                              const double *__restrict__ seg_omT, const double *__restrict__ kappa_s,
+                                              const int32_t *__restrict__ perm, const double *__restrict__ y_s,
+                                              SegRec *__restrict__ rec)
+{
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_seg) return;
+    const int4 sg = seg[g];
+    SegRec r;
+    r.u = sg.x;
+    r.a = sg.y;
+    r.b = sg.z;
+    r.sigma = sg.w;
+    r.h0 = seg_h0[g];
+    r.q0 = seg_q0[g];
+    r.ku = kappa_s[sg.x];
+    r.id_u = perm[sg.x];
+    r.pad = 0;
+    r.yu = model == FM_ECM ? y_s[sg.x] : 0.0;
+    r.omT = seg_omT[g];
+    rec[g] = r;
+}
+
+// test hook (FM_DEBUG_SCRATCH_CAP): every lane-chunk gets the same tiny slot -> forces re-runs
+__global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c <= n_chunks) chunk_cap[c] = c * cap;
 }
 
 }  // namespace fm

@@ -44,38 +44,53 @@ __global__ void k_emit(int model, int64_t n, int64_t n_seg, const double *kappa_
                        const double *ymax, const uint64_t *P, PlanScalars *sc, const RowInfo *rows,
                        const int64_t *row_seg, int4 *seg, double *seg_h0, double *seg_q0, double *seg_omT,
                        int64_t *seg_work);
-__global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg);
+__global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg,
+                         int64_t *chunk_cap);
+__global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap);
+__global__ void k_pack(int model, int64_t n_seg, const int4 *seg, const double *seg_h0, const double *seg_q0,
+                       const double *seg_omT, const double *kappa_s, const int32_t *perm, const double *y_s,
+                       SegRec *rec);
 
 // ------------------------------------------------------------------------------------------
 // sampler (fm_sample.cu)
 // ------------------------------------------------------------------------------------------
 struct SampleArgs {
-    const int4 *seg;
-    const double *seg_h0, *seg_q0, *seg_omT;
+    const SegRec *rec;
     const double *kappa_s, *y_s;
     const int32_t *perm;
-    const int64_t *chunk_seg;
+    const int64_t *chunk_seg;      // [n_chunks+1] first segment of each lane-chunk
+    const int64_t *chunk_cap;      // [n_chunks+1] exclusive prefix of lane-chunk scratch slots (edges)
     int64_t n_chunks;
-    int64_t cap;                // scratch slot per task (edges)
-    uint32_t k0, k1;
+    int64_t cap_per_sample;        // scratch edges per sample (>= chunk_cap[n_chunks])
+    PhiloxKey key;
     uint32_t first_sample;
-    int64_t n_tasks;            // warps launched
-    const int64_t *task_list;   // NULL: task = warp index; else task_list[warp]
-    int2 *edges;                // scratch (normal) or final array (rerun)
-    int32_t *weights;           // ECM
-    const int64_t *rerun_base;  // rerun mode: per-task output base (final offsets); NULL otherwise
-    int64_t *counts;            // [n_samples * n_chunks] edges produced per task (normal mode)
+    int64_t n_tasks;               // tasks in the queue
+    const int64_t *task_list;      // NULL: task = queue index; else task_list[queue index]
+    unsigned long long *task_counter;  // global queue head (zeroed before each launch)
+    int2 *edges;                   // scratch (normal) or final array (rerun)
+    int32_t *weights;              // ECM
+    const int64_t *rerun_base;     // rerun mode: per-task output base (final offsets); NULL otherwise
+    int64_t *counts;               // [n_samples * n_chunks] edges produced per task (normal mode)
+    int2 *spill_e;                 // spill area for tasks that outgrow their slot (one region of
+    int32_t *spill_w;              //   `cap` edges per task, bump-allocated)
+    unsigned long long *spill_counter;
+    int64_t spill_cap;             // edges in the spill area
+    int64_t *spill_off;            // [n_tasks] spill region of each task: -1 none, -2 failed
     unsigned long long *counters;  // draws, landed, accepted
     unsigned int *flags;
 };
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st);
-// tasks whose count exceeds the slot -> overflow list (re-run straight into the final array)
-cudaError_t launch_overflow(int64_t n_tasks, int64_t cap, const int64_t *counts, unsigned long long *n_overflow,
-                            int64_t *overflow_list, cudaStream_t st);
-cudaError_t launch_compact(int64_t n_tasks, int64_t cap, const int64_t *counts, const int64_t *dest,
-                           const int2 *scratch_e, const int32_t *scratch_w, int2 *out_e, int32_t *out_w,
-                           cudaStream_t st);
+// tasks whose count exceeds their slot -> overflow list (re-run straight into the final array)
+cudaError_t launch_overflow(int64_t n_tasks, int64_t n_chunks, const int64_t *chunk_cap, const int64_t *counts,
+                            const int64_t *spill_off, unsigned long long *n_overflow, int64_t *overflow_list,
+                            cudaStream_t st);
+// gather every task's slot (+ spill) into the final contiguous arrays; host passes the total
+cudaError_t launch_compact(int64_t total, int64_t n_tasks, int64_t n_chunks, int64_t cap_per_sample,
+                           const int64_t *chunk_cap, const int64_t *counts, const int64_t *dest,
+                           const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
+                           const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w, cudaStream_t st);
 cudaError_t launch_offsets(int64_t n_samples, int64_t n_chunks, const int64_t *dest, int64_t *offsets, cudaStream_t st);
+cudaError_t launch_debug_eval(int fn, int64_t n, const double *in, double *out, cudaStream_t st);
 
 }  // namespace fm

@@ -26,7 +26,7 @@ FM_FLAG_WEIGHT_SATURATED, FM_FLAG_SCRATCH_RERUN = 1, 2
 STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ERR_CUDA", -4: "FM_ERR_BOUND",
                 -5: "FM_ERR_STATE"}
 SYMBOLS = ["fm_sort_plan", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
-           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get"]
+           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval"]
 
 
 class FastMaxEntError(RuntimeError):
@@ -79,6 +79,8 @@ def _load():
     L.fm_timing_enable.restype = C.c_int
     L.fm_timing_get.argtypes = [C.POINTER(_Timing), C.c_int]
     L.fm_timing_get.restype = C.c_int
+    L.fm_debug_eval.argtypes = [C.c_int32, i64, vp, vp, vp]
+    L.fm_debug_eval.restype = C.c_int
     return L
 
 
@@ -275,3 +277,12 @@ def timing_get(reset: bool = False) -> dict:
     _check(lib.fm_timing_get(C.byref(t), 1 if reset else 0))
     return {"plan_ms": t.plan_ms, "sample_ms": t.sample_ms, "write_ms": t.write_ms,
             "sample_launches": t.sample_launches, "launches": t.launches}
+
+
+def debug_eval(fn: int, x):
+    """fm_debug_eval: the device fp64 logarithms (0 log, 1 log1p, 2 -log(u01(k))) on a CUDA float64 tensor."""
+    import torch
+    x = x.to(device="cuda", dtype=torch.float64).contiguous()
+    out = torch.empty_like(x)
+    _check(lib.fm_debug_eval(int(fn), x.numel(), C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), _stream(None)))
+    return out

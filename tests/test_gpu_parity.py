@@ -44,6 +44,10 @@ def check_parity(O, x, y, S, seed, n_samples, first_sample=0, exact=False, host_
     if bad == 0:
         assert (e.draws, e.landed, e.accepted) == (ref.draws, ref.landed, ref.accepted)
         assert np.array_equal(e.offsets, ref.offsets)
+        # v2 writes every lane-chunk in draw order: the GPU list is the oracle's canonical order
+        assert np.array_equal(E, ref.edges)
+        if W is not None:
+            assert np.array_equal(W, ref.weights)
     return plan, e, ref
 
 
