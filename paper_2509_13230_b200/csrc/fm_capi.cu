@@ -223,6 +223,9 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     uint64_t *ka, *kb;
     int32_t *ia, *ib;
     PlanScalars *sc;
+    unsigned int *hist;
+    CK(tmp.get(&hist, 8 * 256), "alloc hist");
+    CK(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * 8 * 256, st), "memset hist");
     CK(tmp.get(&ka, n), "alloc keys");
     CK(tmp.get(&kb, n), "alloc keys");
     CK(tmp.get(&ia, n), "alloc ids");
@@ -233,7 +236,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     h_sc.key_and = ~0ull;
     CK(cudaMemcpyAsync(sc, &h_sc, sizeof(h_sc), cudaMemcpyHostToDevice, st), "init scalars");
     count_launch();
-    k_validate_key<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, xd, yd, ka, ia, sc);
+    k_validate_key<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, xd, yd, ka, ia, sc, hist);
     CK(cudaGetLastError(), "k_validate_key");
     CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
     CK(cudaStreamSynchronize(st), "sync (validate)");
@@ -258,8 +261,8 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(tmp.get((char **)&work, tmp_bytes), "alloc sort tmp");
     uint64_t *skeys;
     int32_t *perm;
-    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, (uint64_t)(h_sc.key_or ^ h_sc.key_and), &skeys, &perm, work, tmp_bytes,
-                          st),
+    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, (uint64_t)(h_sc.key_or ^ h_sc.key_and), hist, &skeys, &perm, work,
+                          tmp_bytes, st),
        "radix sort");
     tmp.release(perm);
     p->perm = perm;  // adopt the sorted id buffer (freed by plan_release via cudaFree)
@@ -283,9 +286,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(tmp.get(&rows, n), "alloc rows");
     CK(tmp.get(&row_m, n + 1), "alloc row_m");
     count_launch();
-    k_set_F<<<1, 1, 0, st>>>(n, ceil_log2(n), p->kappa_s, sc);
-    count_launch();
-    k_kfx<<<grid_for(n, 256), 256, 0, st>>>(n, p->kappa_s, sc, P);
+    k_kfx<<<grid_for(n, 256), 256, 0, st>>>(n, ceil_log2(n), p->kappa_s, sc, P);
     CK(cudaGetLastError(), "k_kfx");
     CK(scan_exclusive_u64(P, P, n, work, tmp_bytes, st), "scan P");
     count_launch();

@@ -136,9 +136,10 @@ cudaError_t suffix_max_f64(const double *in, double *out, int64_t n, void *tmp, 
 // radix sort (fm_sort.cu): sort (key, val) pairs ascending by key, stable.  Buffers are
 // ping-ponged; on return *key_out/*val_out point to the sorted arrays (one of the two buffers).
 // vary_bits: OR of (key ^ key0) over all keys -- digits with no varying bit are skipped.
+// hist: [8][256] digit counts of every byte position (computed by the caller's key kernel)
 cudaError_t radix_sort_u64_i32(uint64_t *keys_a, uint64_t *keys_b, int32_t *vals_a, int32_t *vals_b, int64_t n,
-                               uint64_t vary_bits, uint64_t **key_out, int32_t **val_out, void *tmp,
-                               size_t tmp_bytes, cudaStream_t st);
+                               uint64_t vary_bits, const unsigned int *hist, uint64_t **key_out, int32_t **val_out,
+                               void *tmp, size_t tmp_bytes, cudaStream_t st);
 size_t radix_tmp_bytes(int64_t n);
 
 }  // namespace fm

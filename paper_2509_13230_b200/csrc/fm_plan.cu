@@ -15,8 +15,13 @@ namespace fm {
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, const double *__restrict__ x,
                                                       const double *__restrict__ y, uint64_t *__restrict__ keys,
-                                                      int32_t *__restrict__ ids, PlanScalars *sc)
+                                                      int32_t *__restrict__ ids, PlanScalars *sc,
+                                                      unsigned int *__restrict__ hist)
 {
+    // also: the radix digit histograms of all 8 byte positions (fm_sort.cu consumes them)
+    __shared__ unsigned int h[8][256];
+    for (int p = 0; p < 8; p++) h[p][threadIdx.x] = 0;
+    __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t kor = 0, kand = ~0ull;
     bool bad = false;
@@ -37,7 +42,12 @@ __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, cons
         kor = key;
         kand = key;
         bad = !ok;
+#pragma unroll
+        for (int p = 0; p < 8; p++) atomicAdd(&h[p][(key >> (8 * p)) & 0xFF], 1u);
     }
+    __syncthreads();
+    for (int p = 0; p < 8; p++)
+        if (h[p][threadIdx.x]) atomicAdd(&hist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kor |= __shfl_xor_sync(0xffffffffu, kor, o);
@@ -71,12 +81,17 @@ __global__ void k_set_F(int64_t n, int L, const double *kappa_s, PlanScalars *sc
     sc->F = 61 - e - L;
 }
 
-__global__ void __launch_bounds__(256) k_kfx(int64_t n, const double *__restrict__ kappa_s,
-                                             const PlanScalars *__restrict__ sc, uint64_t *__restrict__ kfx)
+__global__ void __launch_bounds__(256) k_kfx(int64_t n, int L, const double *__restrict__ kappa_s,
+                                             PlanScalars *__restrict__ sc, uint64_t *__restrict__ kfx)
 {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    kfx[v] = (uint64_t)floor(ldexp(kappa_s[v], sc->F));
+    int e = 0;
+    const double k0 = kappa_s[0];
+    if (k0 > 0.0) frexp(k0, &e);
+    const int F = 61 - e - L;
+    if (v == 0) sc->F = F;
+    kfx[v] = (uint64_t)floor(ldexp(kappa_s[v], F));
 }
 
 // a4 step 3-4 (per row): r_u, sat_u, Wtot_u, m_u

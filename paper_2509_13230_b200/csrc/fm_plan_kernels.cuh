@@ -33,11 +33,11 @@ __device__ __forceinline__ int64_t plan_W(const uint64_t *P, int F, int64_t u, d
 }
 
 __global__ void k_validate_key(int model, int64_t n, const double *x, const double *y, uint64_t *keys, int32_t *ids,
-                               PlanScalars *sc);
+                               PlanScalars *sc, unsigned int *hist);
 __global__ void k_gather_sorted(int model, int64_t n, const uint64_t *skeys, const double *y, const int32_t *perm,
                                 double *kappa_s, double *y_s);
 __global__ void k_set_F(int64_t n, int L, const double *kappa_s, PlanScalars *sc);
-__global__ void k_kfx(int64_t n, const double *kappa_s, const PlanScalars *sc, uint64_t *kfx);
+__global__ void k_kfx(int64_t n, int L, const double *kappa_s, PlanScalars *sc, uint64_t *kfx);
 __global__ void k_rows(int model, int64_t n, int64_t S, const double *kappa_s, const double *y_s, const double *ymax,
                        const uint64_t *P, PlanScalars *sc, RowInfo *rows, int64_t *row_m);
 __global__ void k_emit(int model, int64_t n, int64_t n_seg, const double *kappa_s, const double *y_s,

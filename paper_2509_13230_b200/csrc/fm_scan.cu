@@ -149,22 +149,88 @@ cudaError_t run_scan(const typename Op::T *in, typename Op::T *out, int64_t n, v
 
 __global__ void k_set_f64(double *p, double v) { *p = v; }
 
+// Single-pass exclusive sum (decoupled look-back): tiles in ticket order publish their
+// aggregate, then their inclusive prefix (64-bit status word: 2 flag bits + 62-bit value; all
+// sums here are non-negative and < 2^62).  status[] and the ticket counter start at zero.
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64_t *out, int64_t n,
+                                                      uint64_t *status, unsigned int *ticket)
+{
+    __shared__ unsigned int s_tile;
+    __shared__ uint64_t s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * kTile + (int64_t)threadIdx.x * kItems;
+    uint64_t v[kItems];
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = base + k;
+        v[k] = i < n ? in[i] : 0;
+        acc += v[k];
+    }
+    uint64_t tot;
+    const uint64_t exc = block_exclusive<SumU64>(acc, &tot);
+    if (threadIdx.x == 0) {
+        uint64_t prefix = 0;
+        if (tile == 0) {
+            *(volatile uint64_t *)(status) = kFlagInc | tot;
+        } else {
+            *(volatile uint64_t *)(status + tile) = kFlagAgg | tot;
+            for (int64_t j = tile - 1; j >= 0; j--) {
+                uint64_t w;
+                do {
+                    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(w) : "l"(status + j));
+                } while ((w & ~kValMask) == 0);
+                prefix += w & kValMask;
+                if ((w & ~kValMask) == kFlagInc) break;
+            }
+            *(volatile uint64_t *)(status + tile) = kFlagInc | (prefix + tot);
+        }
+        s_prefix = prefix;
+    }
+    __syncthreads();
+    uint64_t pre = s_prefix + exc;
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+        const int64_t i = base + k;
+        if (i < n) out[i] = pre;
+        pre += v[k];
+    }
+    if (tile == (n - 1) / kTile && threadIdx.x == ((n - 1) % kTile) / kItems) out[n] = pre;  // total
+}
+
+cudaError_t run_scan_lb(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes, cudaStream_t st)
+{
+    const int64_t nb = (n + kTile - 1) / kTile;
+    const size_t need = sizeof(uint64_t) * (size_t)(nb + 1);
+    if (tmp_bytes < need) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(tmp, 0, need, st);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    k_scan_lb<<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, (uint64_t *)tmp, (unsigned int *)((uint64_t *)tmp + nb));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
-size_t scan_tmp_bytes(int64_t n) { return sizeof(int64_t) * (size_t)((n + kTile - 1) / kTile + 1); }
+size_t scan_tmp_bytes(int64_t n) { return sizeof(int64_t) * (size_t)((n + kTile - 1) / kTile + 2); }
 
+// non-negative sums only (all callers): one launch + one memset
 cudaError_t scan_exclusive_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
                                cudaStream_t st)
 {
     if (n == 0) return cudaMemsetAsync(out, 0, sizeof(int64_t), st);
-    return run_scan<SumI64, false, false>(in, out, n, tmp, tmp_bytes, st);
+    return run_scan_lb((const uint64_t *)in, (uint64_t *)out, n, tmp, tmp_bytes, st);
 }
 
 cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
                                cudaStream_t st)
 {
     if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
-    return run_scan<SumU64, false, false>(in, out, n, tmp, tmp_bytes, st);
+    return run_scan_lb(in, out, n, tmp, tmp_bytes, st);
 }
 
 cudaError_t suffix_max_f64(const double *in, double *out, int64_t n, void *tmp, size_t tmp_bytes,

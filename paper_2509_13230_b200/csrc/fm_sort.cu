@@ -1,11 +1,16 @@
-// fm_sort.cu -- a2: stable LSD radix sort of (uint64 key, int32 id) pairs.
+// fm_sort.cu -- a2: stable LSD radix sort of (uint64 key, int32 id) pairs, "one-sweep" style.
 //
 // The sort key is ~bits(kappa): kappa >= 0 doubles order like their bit patterns, so sorting
 // the complement ascending gives kappa descending, and stability keeps ties in ascending id
 // (R9; P:L133 step (i), Alg. 1 line 3).  8-bit digits; a digit none of whose bits
-// varies across the keys is skipped.  Per digit: tile histogram -> exclusive scan (digit-major,
-// so the scan yields each tile's global base per digit) -> stable scatter (warp-level
-// __match_any_sync ranks, cross-warp prefix in shared memory).
+// varies across the keys is skipped.
+//
+// Launches: one memset of the look-back status, then ONE kernel per digit pass (the digit
+// histograms of all positions come with the keys from k_validate_key).  A pass kernel takes tiles in ticket order (atomic counter),
+// ranks its 2048 keys stably (warp __match_any_sync ranks + cross-warp prefix in shared
+// memory), publishes its per-digit counts and resolves its global offsets by decoupled
+// look-back over the preceding tiles (64-bit status words: 2 flag bits + 62-bit count), then
+// scatters.  Each pass reads and writes the keys once (24 B per key).
 #include "fm_internal.cuh"
 
 namespace fm {
@@ -15,36 +20,42 @@ constexpr int kThreads = 256;
 constexpr int kItems = 8;
 constexpr int kTile = kThreads * kItems;  // 2048 keys per tile, 256 per warp
 constexpr int kRadix = 256;
+constexpr int kPasses = 8;
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(kThreads) k_hist(const uint64_t *keys, int64_t n, int shift, int64_t nt,
-                                                   int64_t *counts)
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t *p)
 {
-    __shared__ int h[kRadix];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kTile;
-#pragma unroll
-    for (int k = 0; k < kItems; k++) {
-        const int64_t i = base + (int64_t)k * kThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFF], 1);
-    }
-    __syncthreads();
-    counts[(int64_t)threadIdx.x * nt + blockIdx.x] = h[threadIdx.x];
+    uint64_t v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
 }
 
-__global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
-                                                      uint64_t *__restrict__ kout, int32_t *__restrict__ vout,
-                                                      int64_t n, int shift, int64_t nt,
-                                                      const int64_t *__restrict__ offsets)
+__global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
+                                                   uint64_t *__restrict__ kout, int32_t *__restrict__ vout, int64_t n,
+                                                   int shift, const unsigned int *__restrict__ hist,
+                                                   uint64_t *status, unsigned int *tile_counter)
 {
     __shared__ int wcnt[kThreads / 32][kRadix];
-    __shared__ int64_t tbase[kRadix];
+    __shared__ int64_t s_base[kRadix];
+    __shared__ unsigned int s_wsum[kThreads / 32];
+    __shared__ unsigned int s_tile;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int w = 0; w < kThreads / 32; w++) wcnt[w][threadIdx.x] = 0;
-    tbase[threadIdx.x] = offsets[(int64_t)threadIdx.x * nt + blockIdx.x];
+    // exclusive scan of the pass's global digit counts: the base of each digit
+    unsigned int hv = hist[threadIdx.x], inc = hv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_wsum[wid] = inc;
     __syncthreads();
+    uint64_t dbase = inc - hv;
+    for (int w = 0; w < wid; w++) dbase += s_wsum[w];
+    const int64_t tile = s_tile;
     const uint32_t lt = (1u << lane) - 1u;
-    const int64_t wbase = (int64_t)blockIdx.x * kTile + (int64_t)wid * (kTile / (kThreads / 32));
+    const int64_t wbase = tile * kTile + (int64_t)wid * (kTile / (kThreads / 32));
     uint64_t key[kItems];
     int32_t val[kItems];
     int dig[kItems], loc[kItems];
@@ -64,19 +75,39 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t *__restrict
         __syncwarp();
     }
     __syncthreads();
-    {  // per digit: exclusive prefix over warps (tile-local stable order: warp 0 items first)
+    // thread d: tile-local prefix over warps, the tile's count of digit d, and its global base
+    {
+        const int d = threadIdx.x;
         int acc = 0;
         for (int w = 0; w < kThreads / 32; w++) {
-            const int c = wcnt[w][threadIdx.x];
-            wcnt[w][threadIdx.x] = acc;
+            const int c = wcnt[w][d];
+            wcnt[w][d] = acc;
             acc += c;
         }
+        const uint64_t cnt = (uint64_t)acc;
+        uint64_t *my = status + tile * kRadix + d;
+        uint64_t prefix = 0;
+        if (tile == 0) {
+            *(volatile uint64_t *)my = kFlagInc | cnt;
+        } else {
+            *(volatile uint64_t *)my = kFlagAgg | cnt;
+            for (int64_t j = tile - 1; j >= 0; j--) {
+                uint64_t v;
+                do {
+                    v = ld_volatile_u64(status + j * kRadix + d);
+                } while ((v & ~kValMask) == 0);
+                prefix += v & kValMask;
+                if ((v & ~kValMask) == kFlagInc) break;
+            }
+            *(volatile uint64_t *)my = kFlagInc | (prefix + cnt);
+        }
+        s_base[d] = (int64_t)(dbase + prefix);
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kItems; r++) {
         if (dig[r] < kRadix) {
-            const int64_t dst = tbase[dig[r]] + wcnt[wid][dig[r]] + loc[r];
+            const int64_t dst = s_base[dig[r]] + wcnt[wid][dig[r]] + loc[r];
             kout[dst] = key[r];
             vout[dst] = val[r];
         }
@@ -88,29 +119,27 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t *__restrict
 size_t radix_tmp_bytes(int64_t n)
 {
     const int64_t nt = (n + kTile - 1) / kTile;
-    const int64_t m = nt * kRadix;
-    return sizeof(int64_t) * (size_t)(m + 1) + scan_tmp_bytes(m) + 256;
+    return sizeof(uint64_t) * (size_t)(kPasses * nt * kRadix) + sizeof(unsigned int) * kPasses + 512;
 }
 
 cudaError_t radix_sort_u64_i32(uint64_t *keys_a, uint64_t *keys_b, int32_t *vals_a, int32_t *vals_b, int64_t n,
-                               uint64_t vary_bits, uint64_t **key_out, int32_t **val_out, void *tmp,
-                               size_t tmp_bytes, cudaStream_t st)
+                               uint64_t vary_bits, const unsigned int *hist, uint64_t **key_out, int32_t **val_out,
+                               void *tmp, size_t tmp_bytes, cudaStream_t st)
 {
     const int64_t nt = (n + kTile - 1) / kTile;
-    const int64_t m = nt * kRadix;
     if (tmp_bytes < radix_tmp_bytes(n)) return cudaErrorInvalidValue;
-    int64_t *counts = (int64_t *)tmp;
-    void *scan_tmp = (void *)(((uintptr_t)(counts + m + 1) + 255) & ~(uintptr_t)255);
+    uint64_t *status = (uint64_t *)tmp;
+    unsigned int *tiles = (unsigned int *)(status + kPasses * nt * kRadix);
+    cudaError_t e = cudaMemsetAsync(tmp, 0, radix_tmp_bytes(n) - 512, st);
+    if (e != cudaSuccess) return e;
     uint64_t *ki = keys_a, *ko = keys_b;
     int32_t *vi = vals_a, *vo = vals_b;
-    for (int shift = 0; shift < 64; shift += 8) {
+    for (int p = 0; p < kPasses; p++) {
+        const int shift = 8 * p;
         if (((vary_bits >> shift) & 0xFFull) == 0) continue;
         count_launch();
-        k_hist<<<(unsigned)nt, kThreads, 0, st>>>(ki, n, shift, nt, counts);
-        cudaError_t e = scan_exclusive_i64(counts, counts, m, scan_tmp, scan_tmp_bytes(m), st);
-        if (e != cudaSuccess) return e;
-        count_launch();
-        k_scatter<<<(unsigned)nt, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, nt, counts);
+        k_pass<<<(unsigned)nt, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist + p * kRadix,
+                                                  status + (int64_t)p * nt * kRadix, tiles + p);
         uint64_t *tk = ki; ki = ko; ko = tk;
         int32_t *tv = vi; vi = vo; vo = tv;
     }
