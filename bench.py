@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+from paper_2509_13230_b200 import dist as D  # noqa: E402
 from paper_2509_13230_b200 import workloads as WL  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -56,8 +57,7 @@ def parse():
     return ap.parse_args()
 
 
-def dist_env():
-    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+dist_env = D.env_rank_world
 
 
 # ------------------------------------------------------------------------------------------ clocks
@@ -225,7 +225,7 @@ def run_own(args):
     xd = torch.from_numpy(x).cuda()
     yd = None if y is None else torch.from_numpy(y).cuda()
     R = w.n_samples
-    first = rank * R
+    first, _ = D.shard_samples(rank, world, R)
     sample = fm.sample_ubcm if w.model == "ubcm" else fm.sample_ecm
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -269,16 +269,9 @@ def run_own(args):
     tim = fm.timing_get(reset=True)
     launches = tim["launches"] - l0
     t_rank = sum(ms)
-    if world > 1:
-        tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        cnt = torch.tensor([tot["n_edges"], tot["landed"], tot["draws"], launches], dtype=torch.float64, device="cuda")
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-        t_max = float(tt.item())
-        edges_all, landed_all, draws_all, launches_all = (float(v) for v in cnt.tolist())
-    else:
-        t_max = t_rank
-        edges_all, landed_all, draws_all, launches_all = tot["n_edges"], tot["landed"], tot["draws"], launches
+    t_max = D.reduce_max(t_rank, device="cuda")
+    edges_all, landed_all, draws_all, launches_all = D.reduce_sum(
+        [tot["n_edges"], tot["landed"], tot["draws"], launches], device="cuda")
     value = edges_all / (t_max * 1e-3)
 
     # ---------------- e2e through the C-ABI with host buffers (pinned), copies inside ----------
