@@ -76,7 +76,8 @@ struct fmo_plan {
     int64_t *row_seg; /* first segment of each row, n+1 entries                          */
     int64_t nseg;
     int32_t *seg_u, *seg_a, *seg_b, *seg_sigma;
-    double *seg_h0, *seg_q0, *seg_omT;
+    double *ly_s;     /* ECM: log(y) in rank order (weights, reading R8')                 */
+    double *seg_h0, *seg_x0, *seg_d0, *seg_omT, *seg_iomT;
 };
 
 typedef struct {
@@ -121,7 +122,7 @@ void fmo_plan_free(fmo_plan *p)
     if (!p) return;
     free(p->perm); free(p->kappa_s); free(p->y_s); free(p->ymax); free(p->P); free(p->row_seg);
     free(p->seg_u); free(p->seg_a); free(p->seg_b); free(p->seg_sigma);
-    free(p->seg_h0); free(p->seg_q0); free(p->seg_omT);
+    free(p->ly_s); free(p->seg_h0); free(p->seg_x0); free(p->seg_d0); free(p->seg_omT); free(p->seg_iomT);
     free(p);
 }
 
@@ -147,7 +148,7 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
         keys[i].id = (int32_t)i;
         if (keys[i].kappa > kmax) kmax = keys[i].kappa;
     }
-    if (!isfinite(kmax * kmax)) { free(keys); return FMO_ERR_INVALID; }
+    if (!isfinite((kmax * kmax) * (kmax * kmax))) { free(keys); return FMO_ERR_INVALID; } /* R10 products */
 
     fmo_plan *p = (fmo_plan *)calloc(1, sizeof(fmo_plan));
     if (!p) { free(keys); return FMO_ERR_NOMEM; }
@@ -166,7 +167,10 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
         p->y_s = (double *)malloc(sizeof(double) * (size_t)n);
         p->ymax = (double *)malloc(sizeof(double) * (size_t)(n + 1));
         if (!p->y_s || !p->ymax) goto nomem;
+        p->ly_s = (double *)malloc(sizeof(double) * (size_t)n);
+        if (!p->ly_s) goto nomem;
         for (int64_t r = 0; r < n; r++) p->y_s[r] = y[p->perm[r]];
+        for (int64_t r = 0; r < n; r++) p->ly_s[r] = log(p->y_s[r]);
         p->ymax[n] = 0.0;
         for (int64_t t = n - 1; t >= 0; t--) p->ymax[t] = fmax(p->y_s[t], p->ymax[t + 1]);
     }
@@ -211,9 +215,12 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
     p->seg_b = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nseg + 1));
     p->seg_sigma = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nseg + 1));
     p->seg_h0 = (double *)malloc(sizeof(double) * (size_t)(nseg + 1));
-    p->seg_q0 = (double *)malloc(sizeof(double) * (size_t)(nseg + 1));
+    p->seg_x0 = (double *)malloc(sizeof(double) * (size_t)(nseg + 1));
+    p->seg_d0 = (double *)malloc(sizeof(double) * (size_t)(nseg + 1));
     p->seg_omT = (double *)malloc(sizeof(double) * (size_t)(nseg + 1));
-    if (!p->seg_u || !p->seg_a || !p->seg_b || !p->seg_sigma || !p->seg_h0 || !p->seg_q0 || !p->seg_omT) {
+    p->seg_iomT = (double *)malloc(sizeof(double) * (size_t)(nseg + 1));
+    if (!p->seg_u || !p->seg_a || !p->seg_b || !p->seg_sigma || !p->seg_h0 || !p->seg_x0 || !p->seg_d0 ||
+        !p->seg_omT || !p->seg_iomT) {
         free(m); free(rr); free(sat); free(wtot); goto nomem;
     }
     /* pass 2: cuts and segments */
@@ -244,23 +251,28 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
     }
     free(m); free(rr); free(sat); free(wtot);
     if (bad) { fmo_plan_free(p); return FMO_ERR_STATE; }
-    /* initial bound of every segment at the virtual previous position a-1 (reading R3):
-     * UBCM q = X/(1+X), X = kappa_i kappa_{a-1}; -log(1-q) = log1p(X)            (P:L134)
-     * ECM  q = z/(1-T+z), z = kappa_i kappa_{a-1}, T = y_i ymax[a]; -log(1-q) = log1p(z/(1-T))
-     *                                                                       */
+    /* initial bound of every segment at the virtual previous position a-1 (reading R3), kept as
+     * numerator x0 and denominator d0 of q = x0/d0 (reading R10):
+     * UBCM q = X/(1+X), X = kappa_i kappa_{a-1}; -log(1-q) = log1p(X)               (P:L134)
+     * ECM  q = z/(1-T+z), z = kappa_i kappa_{a-1}, T = y_i ymax[a]; -log(1-q) = log1p(z/(1-T)),
+     *      with z/(1-T) evaluated as z * RN(1/(1-T)) */
     for (int64_t g = 0; g < nseg; g++) {
         int64_t i = p->seg_u[g], a = p->seg_a[g];
         double kq = p->kappa_s[i] * p->kappa_s[a - 1];
+        p->seg_x0[g] = kq;
         if (model == FMO_UBCM) {
             p->seg_omT[g] = 1.0;
-            p->seg_q0[g] = kq / (1.0 + kq);
+            p->seg_iomT[g] = 1.0;
+            p->seg_d0[g] = 1.0 + kq;
             p->seg_h0[g] = log1p(kq);
         } else {
             double T = p->y_s[i] * p->ymax[a];
             double omT = 1.0 - T;
+            double iomT = 1.0 / omT;
             p->seg_omT[g] = omT;
-            p->seg_q0[g] = kq / (omT + kq);
-            p->seg_h0[g] = log1p(kq / omT);
+            p->seg_iomT[g] = iomT;
+            p->seg_d0[g] = omT + kq;
+            p->seg_h0[g] = log1p(kq * iomT);
         }
     }
     *out = p;
@@ -277,7 +289,8 @@ int fmo_plan_F(const fmo_plan *p) { return p->F; }
 
 void fmo_plan_export(const fmo_plan *p, int32_t *perm, double *kappa_s, double *y_s, double *ymax,
                      uint64_t *P, int32_t *seg_u, int32_t *seg_a, int32_t *seg_b, int32_t *seg_sigma,
-                     double *seg_h0, double *seg_q0, double *seg_omT)
+                     double *seg_h0, double *seg_x0, double *seg_d0, double *seg_omT, double *seg_iomT,
+                     double *ly_s)
 {
     size_t n = (size_t)p->n, s = (size_t)p->nseg;
     if (perm) memcpy(perm, p->perm, n * sizeof(int32_t));
@@ -290,8 +303,11 @@ void fmo_plan_export(const fmo_plan *p, int32_t *perm, double *kappa_s, double *
     if (seg_b) memcpy(seg_b, p->seg_b, s * sizeof(int32_t));
     if (seg_sigma) memcpy(seg_sigma, p->seg_sigma, s * sizeof(int32_t));
     if (seg_h0) memcpy(seg_h0, p->seg_h0, s * sizeof(double));
-    if (seg_q0) memcpy(seg_q0, p->seg_q0, s * sizeof(double));
+    if (seg_x0) memcpy(seg_x0, p->seg_x0, s * sizeof(double));
+    if (seg_d0) memcpy(seg_d0, p->seg_d0, s * sizeof(double));
     if (seg_omT) memcpy(seg_omT, p->seg_omT, s * sizeof(double));
+    if (seg_iomT) memcpy(seg_iomT, p->seg_iomT, s * sizeof(double));
+    if (ly_s && p->ly_s) memcpy(ly_s, p->ly_s, n * sizeof(double));
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -374,7 +390,8 @@ static void chain_ubcm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs,
     const uint32_t sigma = (uint32_t)p->seg_sigma[g];
     const double kappa_i = p->kappa_s[i];
     int64_t j = p->seg_a[g] - 1;  /* last evaluated position (virtual a-1 at the start)       */
-    double q = p->seg_q0[g];      /* proposal probability q >= p_ij for every remaining j     */
+    double xq = p->seg_x0[g];     /* proposal q = xq / dq >= p_ij for every remaining j       */
+    double dq = p->seg_d0[g];
     double h = p->seg_h0[g];      /* h = -log(1 - q)                                          */
     const int32_t id_i = p->perm[i];
     for (uint32_t d = 0;; d++) {
@@ -388,17 +405,18 @@ static void chain_ubcm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs,
         if (!(R < (double)(b - 1 - j))) break; /* end of candidate list (R5) */
         j = j + 1 + (int64_t)floor(R);
         out->landed++;
-        /* p_ij = x_i x_j / (1 + x_i x_j)  (P:L92 with x = e^-alpha) */
+        /* p_ij = x_i x_j / (1 + x_i x_j)  (P:L92 with x = e^-alpha), as X / D */
         double X = kappa_i * p->kappa_s[j];
-        double pij = X / (1.0 + X);
-        if (pij > q * (1.0 + 0x1p-50)) out->err = FMO_ERR_STATE; /* contract p <= q */
-        /* accept with probability p/q  (R10) */
-        if (fmo_u01(w_acc) * q < pij) {
+        double D = 1.0 + X;
+        if (X * dq > xq * D * (1.0 + 0x1p-50)) out->err = FMO_ERR_STATE; /* contract p <= q */
+        /* accept with probability p/q: u < (X/D) / (xq/dq), cross-multiplied (R10) */
+        if ((fmo_u01(w_acc) * xq) * D < X * dq) {
             out->accepted++;
             buf_push(out, id_i, p->perm[j], 1);
         }
         /* q <- p_ij; -log(1 - q) = log1p(X) */
-        q = pij;
+        xq = X;
+        dq = D;
         h = log1p(X);
     }
 }
@@ -407,10 +425,12 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
 {
     const int64_t i = p->seg_u[g], b = p->seg_b[g];
     const uint32_t sigma = (uint32_t)p->seg_sigma[g];
-    const double kappa_i = p->kappa_s[i], y_i = p->y_s[i];
-    const double omT = p->seg_omT[g]; /* 1 - exp(-beta_min) for this segment (R6) */
+    const double kappa_i = p->kappa_s[i], y_i = p->y_s[i], ly_i = p->ly_s[i];
+    const double omT = p->seg_omT[g];   /* 1 - exp(-beta_min) for this segment (R6) */
+    const double iomT = p->seg_iomT[g]; /* RN(1 / omT)                                      */
     int64_t j = p->seg_a[g] - 1;
-    double q = p->seg_q0[g];
+    double zq = p->seg_x0[g];          /* q_hat = zq / dq                                  */
+    double dq = p->seg_d0[g];
     double h = p->seg_h0[g];
     const int32_t id_i = p->perm[i];
     for (uint32_t d = 0;; d++) {
@@ -422,14 +442,15 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
         if (!(R < (double)(b - 1 - j))) break;
         j = j + 1 + (int64_t)floor(R);
         out->landed++;
-        /* Eq. 4 in fitness form: z = x_i y_i x_j y_j, t = y_i y_j */
+        /* Eq. 4 in fitness form: p = z / ((1 - t) + z), z = x_i y_i x_j y_j, t = y_i y_j */
         double z = kappa_i * p->kappa_s[j];
         double t = y_i * p->y_s[j];
-        double pij = z / ((1.0 - t) + z);
-        if (pij > q * (1.0 + 0x1p-50)) out->err = FMO_ERR_STATE;
-        if (fmo_u01(W[1]) * q < pij) { /* Alg. 1 line 10 */
-            /* Eq. 5: w - 1 ~ Geometric on {0,1,..} with ratio t; inverse transform (R8) */
-            double G = floor(log(fmo_u01(W[2])) / log(t));
+        double Dp = (1.0 - t) + z;
+        if (z * dq > zq * Dp * (1.0 + 0x1p-50)) out->err = FMO_ERR_STATE;
+        if ((fmo_u01(W[1]) * zq) * Dp < z * dq) { /* Alg. 1 line 10, cross-multiplied (R10) */
+            /* Eq. 5: w - 1 ~ Geometric on {0,1,..} with ratio t = y_i y_j; inverse transform
+             * with log t = log y_i + log y_j (R8) */
+            double G = floor(log(fmo_u01(W[2])) / (ly_i + p->ly_s[j]));
             int32_t w;
             if (G <= 2147483646.0) {
                 w = 1 + (int32_t)G;
@@ -441,8 +462,9 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
             buf_push(out, id_i, p->perm[j], w);
         }
         /* Alg. 1 line 12: q <- p_hat_ij(beta_min) = z / (1 - T + z) (Eq. 6 as equality, R7) */
-        q = z / (omT + z);
-        h = log1p(z / omT);
+        zq = z;
+        dq = omT + z;
+        h = log1p(z * iomT);
     }
 }
 

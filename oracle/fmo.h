@@ -46,7 +46,8 @@ int fmo_plan_F(const fmo_plan *p);
 /* copies of the plan arrays; any pointer may be NULL */
 void fmo_plan_export(const fmo_plan *p, int32_t *perm, double *kappa_s, double *y_s, double *ymax,
                      uint64_t *P, int32_t *seg_u, int32_t *seg_a, int32_t *seg_b, int32_t *seg_sigma,
-                     double *seg_h0, double *seg_q0, double *seg_omT);
+                     double *seg_h0, double *seg_x0, double *seg_d0, double *seg_omT, double *seg_iomT,
+                     double *ly_s);
 
 /* a5-a6: sample.  rows == NULL -> every row; otherwise only the listed sorted-rank rows
  * (ascending, for spot checks at full size).  Edges of each sample are in canonical order

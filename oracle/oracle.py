@@ -65,7 +65,8 @@ def lib():
     L.fmo_plan_nseg.restype = C.c_int64
     L.fmo_plan_F.argtypes = [vp]
     L.fmo_plan_F.restype = C.c_int
-    L.fmo_plan_export.argtypes = [vp, i32p, f64p, f64p, f64p, u64p, i32p, i32p, i32p, i32p, f64p, f64p, f64p]
+    L.fmo_plan_export.argtypes = [vp, i32p, f64p, f64p, f64p, u64p, i32p, i32p, i32p, i32p, f64p, f64p, f64p, f64p,
+                                  f64p, f64p]
     L.fmo_plan_export.restype = None
     L.fmo_sample.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int64, i32p, C.c_int64, C.c_int, C.POINTER(vp)]
     L.fmo_sample.restype = C.c_int
@@ -136,8 +137,11 @@ class Plan:
     seg_b: np.ndarray
     seg_sigma: np.ndarray
     seg_h0: np.ndarray
-    seg_q0: np.ndarray
+    seg_x0: np.ndarray      # numerator of the initial bound q0 = x0 / d0
+    seg_d0: np.ndarray
     seg_omT: np.ndarray
+    seg_iomT: np.ndarray
+    ly_s: np.ndarray | None
     _h: int = 0
 
     @property
@@ -172,13 +176,15 @@ def sort_plan(x, y=None, seg_target: int = 256, model=None) -> Plan:
     ys = np.empty(n, np.float64) if model == ECM else None
     ym = np.empty(n + 1, np.float64) if model == ECM else None
     P = np.empty(n + 1, np.uint64)
+    ly = np.empty(n, np.float64) if model == ECM else None
     su, sa, sb, ss = (np.empty(ns, np.int32) for _ in range(4))
-    h0, q0, om = (np.empty(ns, np.float64) for _ in range(3))
+    h0, x0, d0, om, iom = (np.empty(ns, np.float64) for _ in range(5))
     L.fmo_plan_export(h, _p(perm, C.c_int32), _p(ks, C.c_double), _p(ys, C.c_double), _p(ym, C.c_double),
                       _p(P, C.c_uint64), _p(su, C.c_int32), _p(sa, C.c_int32), _p(sb, C.c_int32),
-                      _p(ss, C.c_int32), _p(h0, C.c_double), _p(q0, C.c_double), _p(om, C.c_double))
-    return Plan(model, n, int(seg_target) or 256, L.fmo_plan_F(h), perm, ks, ys, ym, P, su, sa, sb, ss, h0, q0,
-                om, h.value)
+                      _p(ss, C.c_int32), _p(h0, C.c_double), _p(x0, C.c_double), _p(d0, C.c_double),
+                      _p(om, C.c_double), _p(iom, C.c_double), _p(ly, C.c_double))
+    return Plan(model, n, int(seg_target) or 256, L.fmo_plan_F(h), perm, ks, ys, ym, P, su, sa, sb, ss, h0, x0, d0,
+                om, iom, ly, h.value)
 
 
 @dataclass

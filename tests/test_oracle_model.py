@@ -94,14 +94,29 @@ def test_plan_invariants(O, ecm, S):
     assert np.all(sb[~last] == sa[1:][~last[:-1]])
     assert np.all(sa < sb)
     assert np.all(ss[first] == 0) and np.all(ss[1:][~first[1:]] == ss[:-1][~first[1:]] + 1)
-    # initial bounds (R3): q0 >= p of every candidate of the segment
+    # initial bounds (R3, R10): q0 = x0/d0 at the virtual position a-1 dominates every candidate
     kq = pl.kappa_s[su] * pl.kappa_s[sa - 1]
+    assert np.array_equal(pl.seg_x0, kq)
     if not ecm:
-        assert np.array_equal(pl.seg_q0, kq / (1.0 + kq))
-        assert np.array_equal(pl.seg_h0, np.log1p(kq)) or np.allclose(pl.seg_h0, np.log1p(kq), rtol=4e-16, atol=0)
+        assert np.array_equal(pl.seg_d0, 1.0 + kq)
+        assert np.allclose(pl.seg_h0, np.log1p(kq), rtol=4e-16, atol=0)
+        q0 = kq / (1.0 + kq)
+        for g in range(0, len(su), 97):
+            v = np.arange(sa[g], sb[g])
+            X = pl.kappa_s[su[g]] * pl.kappa_s[v]
+            assert np.all(X / (1.0 + X) <= q0[g] * (1 + 2.0 ** -50))
     else:
         T = pl.y_s[su] * pl.ymax[sa]
         assert np.array_equal(pl.seg_omT, 1.0 - T)
+        assert np.array_equal(pl.seg_iomT, 1.0 / (1.0 - T))
+        assert np.array_equal(pl.seg_d0, (1.0 - T) + kq)
+        assert np.max(np.abs(pl.ly_s.view(np.int64) - np.log(pl.y_s).view(np.int64))) <= 1  # numpy vs glibc log
+        q0 = kq / ((1.0 - T) + kq)
+        for g in range(0, len(su), 97):
+            v = np.arange(sa[g], sb[g])
+            z = pl.kappa_s[su[g]] * pl.kappa_s[v]
+            t = pl.y_s[su[g]] * pl.y_s[v]
+            assert np.all(z / ((1.0 - t) + z) <= q0[g] * (1 + 2.0 ** -50))
 
 
 def test_plan_splits_heavy_rows(O):
@@ -125,7 +140,9 @@ def test_plan_validation(O):
     with pytest.raises(O.OracleError):
         O.sort_plan(np.array([1.0, np.inf]))
     with pytest.raises(O.OracleError):
-        O.sort_plan(np.array([1e200, 1.0]))               # kappa_max^2 overflows
+        O.sort_plan(np.array([1e200, 1.0]))               # kappa_max^4 overflows (R10 products)
+    with pytest.raises(O.OracleError):
+        O.sort_plan(np.array([1e80, 1.0]))
     with pytest.raises(O.OracleError):
         O.sort_plan(np.array([1.0, 1.0]), np.array([0.5, 1.0]))   # y >= 1 (beta <= 0)
     with pytest.raises(O.OracleError):
