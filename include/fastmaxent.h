@@ -36,7 +36,7 @@ extern "C" {
 typedef enum {
     FM_OK = 0,
     FM_ERR_INVALID = -1, /* bad argument: N < 2 or > 2^31-1, NULL pointer, x not finite or < 0,
-                            y not in [0,1), kappa_max^2 overflow, seg_target out of range,
+                            y not in [0,1), kappa_max^4 overflow, seg_target out of range,
                             sample range beyond 2^32 */
     FM_ERR_NOMEM = -2,   /* device or host allocation failed */
     FM_ERR_CUDA = -3,    /* CUDA runtime error (no device, launch failure, ...) */
@@ -113,10 +113,12 @@ fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info);
 
 /* Inspection: copy plan arrays to caller-owned HOST buffers (any may be NULL):
  * perm int32[n] (rank -> id), kappa_s float64[n], y_s float64[n] (ECM), ymax float64[n+1] (ECM),
- * seg int32[4*n_segments] as (u, a, b, sigma), seg_h0/seg_q0/seg_omT float64[n_segments].
- * Synchronises the current device. */
-fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax,
-                         int32_t *seg, double *seg_h0, double *seg_q0, double *seg_omT);
+ * ly_s float64[n] (ECM, log y_s), seg int32[4*n_segments] as (u, a, b, sigma), and per segment
+ * float64[n_segments]: seg_h0 (= -log(1 - q0)), seg_x0 / seg_d0 (q0 = x0 / d0), seg_omT (1 - T),
+ * seg_iomT (RN(1/(1 - T))) -- DESIGN.md 3.4 step 6.  Synchronises the current device. */
+fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax, double *ly_s,
+                         int32_t *seg, double *seg_h0, double *seg_x0, double *seg_d0, double *seg_omT,
+                         double *seg_iomT);
 
 /* Device-side phase timing (for benchmarks).  When enabled, CUDA events are recorded on the
  * call's stream around each phase; fm_timing_get synchronises those events and returns the

@@ -152,10 +152,13 @@ void plan_release(Plan *p)
     cudaFree(p->kappa_s);
     cudaFree(p->y_s);
     cudaFree(p->ymax);
-    cudaFree(p->seg);
-    cudaFree(p->seg_h0);
-    cudaFree(p->seg_q0);
-    cudaFree(p->seg_omT);
+    cudaFree(p->sa.seg);
+    cudaFree(p->sa.h0);
+    cudaFree(p->sa.x0);
+    cudaFree(p->sa.d0);
+    cudaFree(p->sa.omT);
+    cudaFree(p->sa.iomT);
+    cudaFree(p->ly_s);
     cudaFree(p->rec);
     cudaFree(p->chunk_seg);
     cudaFree(p->chunk_cap);
@@ -269,10 +272,12 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(cudaMallocAsync((void **)&p->kappa_s, sizeof(double) * n, st), "alloc kappa_s");
     if (model == FM_ECM) {
         CK(cudaMallocAsync((void **)&p->y_s, sizeof(double) * n, st), "alloc y_s");
+        CK(cudaMallocAsync((void **)&p->ly_s, sizeof(double) * n, st), "alloc ly_s");
         CK(cudaMallocAsync((void **)&p->ymax, sizeof(double) * (n + 1), st), "alloc ymax");
     }
     count_launch();
-    k_gather_sorted<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, skeys, yd, p->perm, p->kappa_s, p->y_s);
+    k_gather_sorted<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, skeys, yd, p->perm, p->kappa_s, p->y_s,
+                                                      p->ly_s);
     CK(cudaGetLastError(), "k_gather_sorted");
 
     // ---- a3: suffix max of y (beta_min) ----
@@ -303,20 +308,22 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     p->wmax = h_sc.wmax;
     p->est_draws = h_sc.total_work >> kG;
     // row_m now holds row_seg (exclusive prefix of the per-row segment counts, n+1 entries)
-    CK(cudaMallocAsync((void **)&p->seg, sizeof(int4) * std::max<int64_t>(n_seg, 1), st), "alloc seg");
-    CK(cudaMallocAsync((void **)&p->seg_h0, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_h0");
-    CK(cudaMallocAsync((void **)&p->seg_q0, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_q0");
-    CK(cudaMallocAsync((void **)&p->seg_omT, sizeof(double) * std::max<int64_t>(n_seg, 1), st), "alloc seg_omT");
+    {
+        const size_t ns = (size_t)std::max<int64_t>(n_seg, 1);
+        CK(cudaMallocAsync((void **)&p->sa.seg, sizeof(int4) * ns, st), "alloc seg");
+        double **arrs[5] = {&p->sa.h0, &p->sa.x0, &p->sa.d0, &p->sa.omT, &p->sa.iomT};
+        for (double **a : arrs) CK(cudaMallocAsync((void **)a, sizeof(double) * ns, st), "alloc seg arrays");
+    }
     int64_t *seg_work;
     CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
     count_launch();
     k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n, n_seg, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
-                                                 row_m, p->seg, p->seg_h0, p->seg_q0, p->seg_omT, seg_work);
+                                                 row_m, p->sa, seg_work);
     CK(cudaGetLastError(), "k_emit");
     CK(cudaMallocAsync((void **)&p->rec, sizeof(SegRec) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
     count_launch();
-    k_pack<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n_seg, p->seg, p->seg_h0, p->seg_q0, p->seg_omT,
-                                                 p->kappa_s, p->perm, p->y_s, p->rec);
+    k_pack<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n_seg, p->sa, p->kappa_s, p->perm, p->y_s, p->ly_s,
+                                                 p->rec);
     CK(cudaGetLastError(), "k_pack");
     {
         const size_t wb = scan_tmp_bytes(n_seg + 1);
@@ -439,6 +446,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.rec = p->rec;
         a.kappa_s = p->kappa_s;
         a.y_s = p->y_s;
+        a.ly_s = p->ly_s;
         a.perm = p->perm;
         a.chunk_seg = p->chunk_seg;
         a.chunk_cap = p->chunk_cap;
@@ -562,8 +570,9 @@ fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info)
     return FM_OK;
 }
 
-fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax, int32_t *seg,
-                         double *seg_h0, double *seg_q0, double *seg_omT)
+fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax, double *ly_s,
+                         int32_t *seg, double *seg_h0, double *seg_x0, double *seg_d0, double *seg_omT,
+                         double *seg_iomT)
 {
     if (!plan || !plan_live(plan)) return fail(FM_ERR_STATE, "not a live fm_plan");
     const Plan *p = (const Plan *)plan;
@@ -573,10 +582,13 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (kappa_s) CK(cudaMemcpy(kappa_s, p->kappa_s, n * 8, cudaMemcpyDeviceToHost), "kappa_s");
     if (y_s && p->y_s) CK(cudaMemcpy(y_s, p->y_s, n * 8, cudaMemcpyDeviceToHost), "y_s");
     if (ymax && p->ymax) CK(cudaMemcpy(ymax, p->ymax, (n + 1) * 8, cudaMemcpyDeviceToHost), "ymax");
-    if (seg && s) CK(cudaMemcpy(seg, p->seg, s * 16, cudaMemcpyDeviceToHost), "seg");
-    if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->seg_h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
-    if (seg_q0 && s) CK(cudaMemcpy(seg_q0, p->seg_q0, s * 8, cudaMemcpyDeviceToHost), "seg_q0");
-    if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->seg_omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
+    if (ly_s && p->ly_s) CK(cudaMemcpy(ly_s, p->ly_s, n * 8, cudaMemcpyDeviceToHost), "ly_s");
+    if (seg && s) CK(cudaMemcpy(seg, p->sa.seg, s * 16, cudaMemcpyDeviceToHost), "seg");
+    if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->sa.h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
+    if (seg_x0 && s) CK(cudaMemcpy(seg_x0, p->sa.x0, s * 8, cudaMemcpyDeviceToHost), "seg_x0");
+    if (seg_d0 && s) CK(cudaMemcpy(seg_d0, p->sa.d0, s * 8, cudaMemcpyDeviceToHost), "seg_d0");
+    if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->sa.omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
+    if (seg_iomT && s) CK(cudaMemcpy(seg_iomT, p->sa.iomT, s * 8, cudaMemcpyDeviceToHost), "seg_iomT");
     return FM_OK;
 }
 

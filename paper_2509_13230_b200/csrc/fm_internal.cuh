@@ -21,13 +21,20 @@ enum : uint32_t {
     kFlagWeightSat = 8u,  // ECM weight clamped
 };
 
-// one plan segment as the sampler reads it (64 B, two halves of 32 B; UBCM reads the first 48 B)
+// one plan segment as the sampler reads it (96 B in 16-byte parts; UBCM reads the first 64 B)
 struct __align__(16) SegRec {
     int32_t u, a, b, sigma;  // focal rank, candidates [a, b), segment index in the row
-    double h0, q0;           // initial bound at a-1: h0 = -log(1 - q0), q0
-    double ku;               // kappa_s[u]
-    int32_t id_u, pad;       // perm[u]
-    double yu, omT;          // ECM: y_s[u], 1 - T
+    double h0, x0;           // initial bound at a-1: q0 = x0 / d0, h0 = -log(1 - q0)
+    double d0, ku;           // ..., kappa_s[u]
+    int32_t id_u, pad0, pad1, pad2;  // perm[u]
+    double yu, ly_u;         // ECM: y_s[u], log y_s[u]
+    double omT, iomT;        // ECM: 1 - T, RN(1 / (1 - T))
+};
+
+// per-segment plan arrays (SoA, exported for tests; k_pack builds SegRec from them)
+struct SegArrays {
+    int4 *seg;  // (u, a, b, sigma)
+    double *h0, *x0, *d0, *omT, *iomT;
 };
 
 struct Plan {
@@ -43,10 +50,8 @@ struct Plan {
     double *ymax;       // [n+1] ECM
     // a4 segments
     int64_t n_seg;
-    int4 *seg;          // [n_seg] (u, a, b, sigma)
-    double *seg_h0;     // [n_seg]
-    double *seg_q0;     // [n_seg]
-    double *seg_omT;    // [n_seg] ECM (1.0 for UBCM)
+    SegArrays sa;       // [n_seg] each
+    double *ly_s;       // [n] ECM: log y_s
     SegRec *rec;        // [n_seg] packed copy of the above for the sampler
     int64_t est_draws;  // sum of segment work estimates / 2^G
     // chunking (does not change results)

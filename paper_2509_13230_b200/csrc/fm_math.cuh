@@ -30,13 +30,12 @@ struct LogTable {
     double logc_lo[kLogTable];  // logc - logc_hi (|.| < 2^-44)
 };
 
-// polynomial coefficients and ln2 split (the including TU keeps them in the constant bank, written
-// at run time, so DFMA reads them as c[][] operands instead of materialising 64-bit immediates)
+// polynomial coefficients and ln2 split (compile-time constants: materialised as immediates)
 struct LogConsts {
     double c3, c5, c6, c7;  // 1/3, 1/5, 1/6, 1/7
     double ln2_hi, ln2_lo;  // LN2_HI has 11 trailing zero bits: k * LN2_HI is exact for |k| < 2^11
 };
-inline LogConsts log_consts()
+__host__ __device__ __forceinline__ constexpr LogConsts log_consts()
 {
     return {0x1.5555555555555p-2, 0.2, 0x1.5555555555555p-3, 0x1.2492492492492p-3, 0x1.62e42fefa3800p-1,
             0x1.ef35793c76730p-45};
@@ -56,7 +55,7 @@ __device__ __forceinline__ double fm_log_core(double x, double c, const Tab &T)
     const double kd = (double)k;
     const double2 icv = T.ic(i);
     const double invc = icv.x, lc_hi = icv.y, lc_lo = T.lo(i);
-    const LogConsts &K = T.C();
+    const LogConsts K = T.C();
     // r = z * invc - 1 exactly, as r + p_lo
     const double p_hi = __dmul_rn(z, invc);
     const double p_lo = __fma_rn(z, invc, -p_hi);

@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, cons
             kappa = __dmul_rn(xi, yi);
         }
         kappa = __dadd_rn(kappa, 0.0);  // -0.0 -> +0.0
-        ok = ok && isfinite(__dmul_rn(kappa, kappa));
+        const double k2 = __dmul_rn(kappa, kappa);
+        ok = ok && isfinite(__dmul_rn(k2, k2));  // R10's cross products stay finite
         const uint64_t key = ~(uint64_t)__double_as_longlong(kappa);
         keys[i] = key;
         ids[i] = (int32_t)i;
@@ -64,12 +65,17 @@ __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, cons
 // a2 epilogue: rank-space arrays from the sorted keys
 __global__ void __launch_bounds__(256) k_gather_sorted(int model, int64_t n, const uint64_t *__restrict__ skeys,
                                                        const double *__restrict__ y, const int32_t *__restrict__ perm,
-                                                       double *__restrict__ kappa_s, double *__restrict__ y_s)
+                                                       double *__restrict__ kappa_s, double *__restrict__ y_s,
+                                                       double *__restrict__ ly_s)
 {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     kappa_s[r] = __longlong_as_double((long long)~skeys[r]);
-    if (model == FM_ECM) y_s[r] = y[perm[r]];
+    if (model == FM_ECM) {
+        const double yr = y[perm[r]];
+        y_s[r] = yr;
+        ly_s[r] = log(yr);  // R8: log t = log y_i + log y_j
+    }
 }
 
 // a4 step 1-2: F and the fixed-point keys
@@ -161,9 +167,7 @@ __global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_se
                                               const double *__restrict__ y_s, const double *__restrict__ ymax,
                                               const uint64_t *__restrict__ P, PlanScalars *sc,
                                               const RowInfo *__restrict__ rows, const int64_t *__restrict__ row_seg,
-                                              int4 *__restrict__ seg,
-                                              double *__restrict__ seg_h0, double *__restrict__ seg_q0,
-                                              double *__restrict__ seg_omT, int64_t *__restrict__ seg_work)
+                                              SegArrays sa, int64_t *__restrict__ seg_work)
 {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_seg) return;
@@ -183,18 +187,22 @@ __global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_se
     a = sigma == 0 ? u + 1 : plan_cut(P, F, n, u, ri, m, sigma);
     b = sigma == m - 1 ? n : plan_cut(P, F, n, u, ri, m, sigma + 1);
     if (!(a < b) || !(a > u)) atomicOr(&sc->flags, kErrState);
-    seg[g] = make_int4((int)u, (int)a, (int)b, (int)sigma);
+    sa.seg[g] = make_int4((int)u, (int)a, (int)b, (int)sigma);
     const double kq = __dmul_rn(kappa_s[u], kappa_s[a - 1]);
+    sa.x0[g] = kq;
     if (model == FM_UBCM) {
-        seg_omT[g] = 1.0;
-        seg_q0[g] = __ddiv_rn(kq, __dadd_rn(1.0, kq));
-        seg_h0[g] = log1p(kq);
+        sa.omT[g] = 1.0;
+        sa.iomT[g] = 1.0;
+        sa.d0[g] = __dadd_rn(1.0, kq);
+        sa.h0[g] = log1p(kq);
     } else {
         const double T = __dmul_rn(y_s[u], ymax[a]);
         const double omT = __dsub_rn(1.0, T);
-        seg_omT[g] = omT;
-        seg_q0[g] = __ddiv_rn(kq, __dadd_rn(omT, kq));
-        seg_h0[g] = log1p(__ddiv_rn(kq, omT));
+        const double iomT = __ddiv_rn(1.0, omT);
+        sa.omT[g] = omT;
+        sa.iomT[g] = iomT;
+        sa.d0[g] = __dadd_rn(omT, kq);
+        sa.h0[g] = log1p(__dmul_rn(kq, iomT));
     }
     const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, u, ri.r, ri.sat, a);
     const int64_t wb = plan_W(P, F, u, ri.r, ri.sat, b);
@@ -226,28 +234,29 @@ __global__ void __launch_bounds__(256) k_chunks(int64_t n_seg, int64_t n_chunks,
     chunk_cap[c] = ((w + (w >> 2)) >> kG) + 16;
 }
 
-// packed per-segment records for the sampler (one 64-byte load instead of five gathers)
-__global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, const int4 *__restrict__ seg,
-                                              const double *__restrict__ seg_h0, const double *__restrict__ seg_q0,
-                                              const double *__restrict__ seg_omT, const double *__restrict__ kappa_s,
+// packed per-segment records for the sampler (one 64/96-byte read instead of eight gathers)
+__global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, SegArrays sa, const double *__restrict__ kappa_s,
                                               const int32_t *__restrict__ perm, const double *__restrict__ y_s,
-                                              SegRec *__restrict__ rec)
+                                              const double *__restrict__ ly_s, SegRec *__restrict__ rec)
 {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_seg) return;
-    const int4 sg = seg[g];
+    const int4 sg = sa.seg[g];
     SegRec r;
     r.u = sg.x;
     r.a = sg.y;
     r.b = sg.z;
     r.sigma = sg.w;
-    r.h0 = seg_h0[g];
-    r.q0 = seg_q0[g];
+    r.h0 = sa.h0[g];
+    r.x0 = sa.x0[g];
+    r.d0 = sa.d0[g];
     r.ku = kappa_s[sg.x];
     r.id_u = perm[sg.x];
-    r.pad = 0;
+    r.pad0 = r.pad1 = r.pad2 = 0;
     r.yu = model == FM_ECM ? y_s[sg.x] : 0.0;
-    r.omT = seg_omT[g];
+    r.ly_u = model == FM_ECM ? ly_s[sg.x] : 0.0;
+    r.omT = sa.omT[g];
+    r.iomT = sa.iomT[g];
     rec[g] = r;
 }
 

@@ -35,28 +35,26 @@ __device__ __forceinline__ int64_t plan_W(const uint64_t *P, int F, int64_t u, d
 __global__ void k_validate_key(int model, int64_t n, const double *x, const double *y, uint64_t *keys, int32_t *ids,
                                PlanScalars *sc, unsigned int *hist);
 __global__ void k_gather_sorted(int model, int64_t n, const uint64_t *skeys, const double *y, const int32_t *perm,
-                                double *kappa_s, double *y_s);
+                                double *kappa_s, double *y_s, double *ly_s);
 __global__ void k_set_F(int64_t n, int L, const double *kappa_s, PlanScalars *sc);
 __global__ void k_kfx(int64_t n, int L, const double *kappa_s, PlanScalars *sc, uint64_t *kfx);
 __global__ void k_rows(int model, int64_t n, int64_t S, const double *kappa_s, const double *y_s, const double *ymax,
                        const uint64_t *P, PlanScalars *sc, RowInfo *rows, int64_t *row_m);
 __global__ void k_emit(int model, int64_t n, int64_t n_seg, const double *kappa_s, const double *y_s,
                        const double *ymax, const uint64_t *P, PlanScalars *sc, const RowInfo *rows,
-                       const int64_t *row_seg, int4 *seg, double *seg_h0, double *seg_q0, double *seg_omT,
-                       int64_t *seg_work);
+                       const int64_t *row_seg, SegArrays sa, int64_t *seg_work);
 __global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg,
                          int64_t *chunk_cap);
 __global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap);
-__global__ void k_pack(int model, int64_t n_seg, const int4 *seg, const double *seg_h0, const double *seg_q0,
-                       const double *seg_omT, const double *kappa_s, const int32_t *perm, const double *y_s,
-                       SegRec *rec);
+__global__ void k_pack(int model, int64_t n_seg, SegArrays sa, const double *kappa_s, const int32_t *perm,
+                       const double *y_s, const double *ly_s, SegRec *rec);
 
 // ------------------------------------------------------------------------------------------
 // sampler (fm_sample.cu)
 // ------------------------------------------------------------------------------------------
 struct SampleArgs {
     const SegRec *rec;
-    const double *kappa_s, *y_s;
+    const double *kappa_s, *y_s, *ly_s;
     const int32_t *perm;
     const int64_t *chunk_seg;      // [n_chunks+1] first segment of each lane-chunk
     const int64_t *chunk_cap;      // [n_chunks+1] exclusive prefix of lane-chunk scratch slots (edges)

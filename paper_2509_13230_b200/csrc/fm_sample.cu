@@ -18,6 +18,7 @@
 #include <float.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "fm_internal.cuh"
@@ -27,11 +28,11 @@
 namespace fm {
 
 __device__ LogTable g_logtab;
-__constant__ LogConsts c_log;  // written by ensure_log_table (not folded: read as c[][] operands)
 
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kBatch = 64;  // tasks per warp batch
 
 // per-block copy of the log table (file-scope shared: addressed with constant offsets)
 __shared__ double2 s_log_ic[kLogTable];
@@ -39,7 +40,7 @@ __shared__ double s_log_lo[kLogTable];
 struct SmemLogTab {
     __device__ __forceinline__ double2 ic(int i) const { return s_log_ic[i]; }
     __device__ __forceinline__ double lo(int i) const { return s_log_lo[i]; }
-    __device__ __forceinline__ const LogConsts &C() const { return c_log; }
+    __device__ __forceinline__ LogConsts C() const { return log_consts(); }
 };
 
 __device__ __forceinline__ void load_logtab()
@@ -51,8 +52,8 @@ __device__ __forceinline__ void load_logtab()
     __syncthreads();
 }
 
-template <int kModel>
-__global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
+template <int kModel, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
     __shared__ SegRec s_next[kThreads];
     load_logtab();
@@ -62,6 +63,10 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
 
     // ---- task (lane-chunk) state ----
     int64_t task = -1, slot = 0, sp = -1;
+    // warp batch of task ids [bpos, bend); lane 0 holds the start of the next batch
+    unsigned long long next_batch = 0;
+    if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
+    int64_t bpos = 0, bend = 0;
     int32_t g = 0, g_end = 0, cnt = 0, cap = 0;
     uint32_t s_abs = 0;
     bool warp_done = false;
@@ -69,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
     bool act = false;
     int32_t u = 0, b = 0, cur = 0, id_u = 0;
     uint32_t sg = 0, d = 0;
-    double q = 0.0, h = 0.0, ku = 0.0, yu = 0.0, omT = 1.0, E = 0.0;
+    double xq = 0.0, dq = 1.0, h = 0.0, ku = 0.0, yu = 0.0, lyu = 0.0, omT = 1.0, iomT = 1.0, E = 0.0;
     uint32_t wacc = 0, wwt = 0;
     // ---- counters ----
     uint32_t n_draw = 0, n_land = 0, n_acc = 0;
@@ -81,45 +86,40 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
     SegRec *my_next = &s_next[threadIdx.x];
     const uint32_t my_next_sa = (uint32_t)__cvta_generic_to_shared(my_next);
     auto start_seg = [&](bool prefetched) {
-        int4 h4;
-        double2 b2, c2, d2 = make_double2(0.0, 1.0);
-        if (prefetched) {
-            asm volatile("cp.async.wait_all;\n" ::: "memory");
-            h4 = *reinterpret_cast<const int4 *>(my_next);
-            b2 = *reinterpret_cast<const double2 *>(&my_next->h0);
-            c2 = *reinterpret_cast<const double2 *>(&my_next->ku);
-            if (kModel == FM_ECM) d2 = *reinterpret_cast<const double2 *>(&my_next->yu);
-        } else {
-            const SegRec *r = A.rec + g;
-            h4 = *reinterpret_cast<const int4 *>(r);
-            b2 = *reinterpret_cast<const double2 *>(&r->h0);
-            c2 = *reinterpret_cast<const double2 *>(&r->ku);
-            if (kModel == FM_ECM) d2 = *reinterpret_cast<const double2 *>(&r->yu);
-        }
-        u = h4.x;
-        cur = h4.y - 1;  // virtual previous position a-1 (R3)
-        b = h4.z;
-        sg = (uint32_t)h4.w;
-        h = b2.x;
-        q = b2.y;
-        ku = c2.x;
-        id_u = __double2loint(c2.y);
+        const SegRec *r = prefetched ? my_next : A.rec + g;
+        if (prefetched) asm volatile("cp.async.wait_all;\n" ::: "memory");
+        const int4 p0 = *reinterpret_cast<const int4 *>(r);
+        const double2 p1 = *reinterpret_cast<const double2 *>(&r->h0);
+        const double2 p2 = *reinterpret_cast<const double2 *>(&r->d0);
+        const int4 p3 = *reinterpret_cast<const int4 *>(&r->id_u);
+        u = p0.x;
+        cur = p0.y - 1;  // virtual previous position a-1 (R3)
+        b = p0.z;
+        sg = (uint32_t)p0.w;
+        h = p1.x;
+        xq = p1.y;
+        dq = p2.x;
+        ku = p2.y;
+        id_u = p3.x;
         if (kModel == FM_ECM) {
-            yu = d2.x;
-            omT = d2.y;
+            const double2 p4 = *reinterpret_cast<const double2 *>(&r->yu);
+            const double2 p5 = *reinterpret_cast<const double2 *>(&r->omT);
+            yu = p4.x;
+            lyu = p4.y;
+            omT = p5.x;
+            iomT = p5.y;
         }
         d = 0;
         g++;
         act = true;
         if (g < g_end) {
             const char *src = reinterpret_cast<const char *>(A.rec + g);
-            const int parts = kModel == FM_ECM ? 4 : 3;
+            constexpr int parts = kModel == FM_ECM ? 6 : 4;
 #pragma unroll
-            for (int k = 0; k < 4; k++)
-                if (k < parts)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(my_next_sa + 16 * k),
-                                 "l"(src + 16 * k)
-                                 : "memory");
+            for (int k = 0; k < parts; k++)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(my_next_sa + 16 * k),
+                             "l"(src + 16 * k)
+                             : "memory");
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
     };
@@ -140,6 +140,9 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
 
     for (;;) {
         // ---- 1. task management (lanes whose task has no segment left) ----
+        // Tasks come in warp batches of kBatch consecutive ids from the global queue; the next
+        // batch is requested (by lane 0) as soon as the current one is opened, so the atomic's
+        // latency is never waited for.
         const bool needc = !act;
         if (needc && task >= 0) {
             if (!A.rerun_base) {
@@ -151,35 +154,41 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
         const uint32_t nc = __ballot_sync(0xffffffffu, needc && !warp_done);
         bool fresh = false;
         if (nc) {
-            const int leader = __ffs(nc) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(A.task_counter, (unsigned long long)__popc(nc));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (needc && !warp_done) {
-                const int64_t my = (int64_t)base + __popc(nc & lt);
-                if (my < A.n_tasks) {
-                    const int64_t t = A.task_list ? A.task_list[my] : my;
-                    const int64_t s = t / A.n_chunks, c = t - s * A.n_chunks;
-                    task = t;
-                    g = (int32_t)A.chunk_seg[c];
-                    g_end = (int32_t)A.chunk_seg[c + 1];
-                    if (A.rerun_base) {
-                        slot = A.rerun_base[t];
-                        cap = INT32_MAX;
-                    } else {
-                        slot = s * A.cap_per_sample + A.chunk_cap[c];
-                        cap = (int32_t)(A.chunk_cap[c + 1] - A.chunk_cap[c]);
-                    }
-                    s_abs = A.first_sample + (uint32_t)s;
-                    cnt = 0;
-                    sp = -1;
-                    if (g < g_end) {
-                        start_seg(false);
-                        fresh = true;
-                    }
+            const int k = __popc(nc), rank = __popc(nc & lt);
+            const int64_t avail = bend - bpos;
+            int64_t my;
+            if (k <= avail) {
+                my = bpos + rank;
+                bpos += k;
+            } else {
+                const int64_t nb = (int64_t)__shfl_sync(0xffffffffu, next_batch, 0);
+                my = rank < avail ? bpos + rank : nb + (rank - avail);
+                bpos = nb + (k - avail);
+                bend = nb + kBatch;
+                if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
+            }
+            if (needc && !warp_done && my < A.n_tasks) {
+                const int64_t t = A.task_list ? A.task_list[my] : my;
+                const int64_t s = t / A.n_chunks, c = t - s * A.n_chunks;
+                task = t;
+                g = (int32_t)A.chunk_seg[c];
+                g_end = (int32_t)A.chunk_seg[c + 1];
+                if (A.rerun_base) {
+                    slot = A.rerun_base[t];
+                    cap = INT32_MAX;
+                } else {
+                    slot = s * A.cap_per_sample + A.chunk_cap[c];
+                    cap = (int32_t)(A.chunk_cap[c + 1] - A.chunk_cap[c]);
+                }
+                s_abs = A.first_sample + (uint32_t)s;
+                cnt = 0;
+                sp = -1;
+                if (g < g_end) {
+                    start_seg(false);
+                    fresh = true;
                 }
             }
-            if ((int64_t)base + __popc(nc) >= A.n_tasks) warp_done = true;
+            if (bpos >= A.n_tasks) warp_done = true;
         }
         if (!__any_sync(0xffffffffu, act)) {
             if (warp_done) break;
@@ -191,7 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
         // ---- 3. consume one draw ----
         bool landed = false;
         uint32_t w_land = 0, w_wt = 0;
-        double kv = 0.0, yv = 0.0;
+        double kv = 0.0, yv = 0.0, lyv = 0.0;
         int32_t id_v = 0;
         if (act) {
             n_draw++;
@@ -202,7 +211,10 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
             } else {
                 cur = cur + 1 + (int32_t)R;  // R >= 0: truncation == floor
                 kv = A.kappa_s[cur];
-                if (kModel == FM_ECM) yv = A.y_s[cur];
+                if (kModel == FM_ECM) {
+                    yv = A.y_s[cur];
+                    lyv = A.ly_s[cur];
+                }
                 id_v = A.perm[cur];  // issued early; needed only if accepted
                 landed = true;
                 w_land = wacc;
@@ -230,28 +242,32 @@ __global__ void __launch_bounds__(kThreads) k_sample(const SampleArgs A)
             }
             const double Enew = -fm_log(u01(ws), T);
             if (kModel == FM_UBCM) {
-                const double X = landed ? __dmul_rn(ku, kv) : 1.0;  // dummy: keeps __ddiv_rn on its fast path
-                const double p = __ddiv_rn(X, __dadd_rn(1.0, X));
+                // (kv + 0*Enew) orders the use of the gathered kv after the RNG/log work above,
+                // so the gather latency hides behind it; exact since Enew is finite and kv >= 0
+                const double kvd = __dadd_rn(kv, __dmul_rn(Enew, 0.0));
+                const double X = landed ? __dmul_rn(ku, kvd) : 1.0;  // dummy for restarted lanes
+                const double D = __dadd_rn(1.0, X);
                 const double hn = fm_log1p(X, T);
-                if (landed) {
-                    acc = __dmul_rn(u01(w_land), q) < p;
-                    q = p;
+                if (landed) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
+                    acc = __dmul_rn(__dmul_rn(u01(w_land), xq), D) < __dmul_rn(X, dq);
+                    xq = X;
+                    dq = D;
                     h = hn;
                 }
             } else {
-                const double z = landed ? __dmul_rn(ku, kv) : 1.0;  // dummy: keeps __ddiv_rn on its fast path
+                const double kvd = __dadd_rn(kv, __dmul_rn(Enew, 0.0));  // see UBCM
+                const double z = landed ? __dmul_rn(ku, kvd) : 1.0;  // dummy for restarted lanes
                 const double t = __dmul_rn(yu, yv);
-                const double p = __ddiv_rn(z, __dadd_rn(__dsub_rn(1.0, t), z));
-                const double qn = __ddiv_rn(z, __dadd_rn(omT, z));
-                const double hn = fm_log1p(__ddiv_rn(z, omT), T);
+                const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
+                const double hn = fm_log1p(__dmul_rn(z, iomT), T);
                 if (landed) {
-                    acc = __dmul_rn(u01(w_land), q) < p;
-                    q = qn;
+                    acc = __dmul_rn(__dmul_rn(u01(w_land), xq), Dp) < __dmul_rn(z, dq);
+                    xq = z;
+                    dq = __dadd_rn(omT, z);
                     h = hn;
-                    if (acc) {
+                    if (acc) {  // Eq. 5 weight, log t = log y_u + log y_v (R8)
                         const double lu = fm_log(u01(w_wt), T);
-                        const double ltt = t >= DBL_MIN ? fm_log(t, T) : log(t);
-                        const double G = floor(__ddiv_rn(lu, ltt));
+                        const double G = floor(__ddiv_rn(lu, __dadd_rn(lyu, lyv)));
                         if (G <= 2147483646.0) {
                             w = 1 + (int32_t)G;
                         } else {
@@ -447,23 +463,37 @@ cudaError_t ensure_log_table(cudaStream_t st)
     std::lock_guard<std::mutex> lk(g_tab_mu);
     if (dev < 64 && g_tab_done[dev]) return cudaSuccess;
     static const LogTable T = make_log_table();
-    static const LogConsts K = log_consts();
     e = cudaMemcpyToSymbol(g_logtab, &T, sizeof(T));
-    if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_log, &K, sizeof(K));
     if (e == cudaSuccess && dev < 64) g_tab_done[dev] = true;
     return e;
 }
 
-int sample_blocks(int model)
+// the sampler is instantiated for several register budgets (min resident blocks per SM);
+// FM_SAMPLE_MINB selects one at run time (tuning), default per model
+template <int kModel, int kMinB>
+static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (model == FM_UBCM)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<FM_UBCM>, kThreads, 0);
-    else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<FM_ECM>, kThreads, 0);
-    return sms * (per > 0 ? per : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB>, kThreads, 0);
+    int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
+    const int64_t need = (a.n_tasks + kThreads - 1) / kThreads;  // at most one task per lane at start
+    if (need < blocks) blocks = need;
+    count_launch();
+    k_sample<kModel, kMinB><<<(unsigned)blocks, kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int kModel>
+static cudaError_t launch_sample_m(int minb, const SampleArgs &a, cudaStream_t st)
+{
+    switch (minb) {
+    case 1: return launch_sample_t<kModel, 1>(a, st);
+    case 2: return launch_sample_t<kModel, 2>(a, st);
+    case 4: return launch_sample_t<kModel, 4>(a, st);
+    default: return launch_sample_t<kModel, 3>(a, st);
+    }
 }
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
@@ -477,15 +507,9 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
         e = cudaMemsetAsync(a.spill_counter, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
     }
-    int64_t blocks = sample_blocks(model);
-    const int64_t need = (a.n_tasks + kThreads - 1) / kThreads;  // at most one task per lane at start
-    if (need < blocks) blocks = need;
-    count_launch();
-    if (model == FM_UBCM)
-        k_sample<FM_UBCM><<<(unsigned)blocks, kThreads, 0, st>>>(a);
-    else
-        k_sample<FM_ECM><<<(unsigned)blocks, kThreads, 0, st>>>(a);
-    return cudaGetLastError();
+    const char *ev = getenv("FM_SAMPLE_MINB");
+    const int minb = ev && *ev ? atoi(ev) : (model == FM_UBCM ? 3 : 2);
+    return model == FM_UBCM ? launch_sample_m<FM_UBCM>(minb, a, st) : launch_sample_m<FM_ECM>(minb, a, st);
 }
 
 cudaError_t launch_overflow(int64_t n_tasks, int64_t n_chunks, const int64_t *chunk_cap, const int64_t *counts,

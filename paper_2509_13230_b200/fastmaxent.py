@@ -67,7 +67,7 @@ def _load():
     L.fm_edges_to_host.restype = C.c_int
     L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
     L.fm_plan_get_info.restype = C.c_int
-    L.fm_plan_export.argtypes = [vp] + [vp] * 8
+    L.fm_plan_export.argtypes = [vp] + [vp] * 11
     L.fm_plan_export.restype = C.c_int
     L.fm_free.argtypes = [vp]
     L.fm_free.restype = None
@@ -144,13 +144,14 @@ class Plan:
     def export(self) -> dict:
         n, s = self.n, self.n_segments
         ecm = self.model == FM_ECM
+        keys = ("perm", "kappa_s", "y_s", "ymax", "ly_s", "seg", "seg_h0", "seg_x0", "seg_d0", "seg_omT", "seg_iomT")
         out = {"perm": np.empty(n, np.int32), "kappa_s": np.empty(n, np.float64),
                "y_s": np.empty(n, np.float64) if ecm else None, "ymax": np.empty(n + 1, np.float64) if ecm else None,
-               "seg": np.empty((s, 4), np.int32), "seg_h0": np.empty(s), "seg_q0": np.empty(s),
-               "seg_omT": np.empty(s)}
+               "ly_s": np.empty(n, np.float64) if ecm else None, "seg": np.empty((s, 4), np.int32)}
+        for k in keys[6:]:
+            out[k] = np.empty(s)
         ptr = lambda a: None if a is None else C.c_void_p(a.ctypes.data)  # noqa: E731
-        _check(lib.fm_plan_export(self._h, *(ptr(out[k]) for k in ("perm", "kappa_s", "y_s", "ymax", "seg", "seg_h0",
-                                                                    "seg_q0", "seg_omT"))))
+        _check(lib.fm_plan_export(self._h, *(ptr(out[k]) for k in keys)))
         return out
 
     def free(self):

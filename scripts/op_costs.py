@@ -65,13 +65,17 @@ def main():
                   o["u01"]["fp64"] + o["log"]["fp64"] + o["ddiv"]["fp64"] + 2)
     draw_e = unit(ph_e + o["u01"]["inst"] + o["log"]["inst"] + o["ddiv"]["inst"] + 4,
                   o["u01"]["fp64"] + o["log"]["fp64"] + o["ddiv"]["fp64"] + 2)
-    land_u = unit(1 + 2 + 2 + 2 + o["ddiv"]["inst"] + o["u01"]["inst"] + 2 + o["log1p"]["inst"],
-                  1 + 2 + o["ddiv"]["fp64"] + o["u01"]["fp64"] + 2 + o["log1p"]["fp64"])
-    land_e = unit(1 + 2 + 4 + 4 + 3 * o["ddiv"]["inst"] + o["u01"]["inst"] + 2 + 1 + o["log1p"]["inst"],
-                  1 + 4 + 3 * o["ddiv"]["fp64"] + o["u01"]["fp64"] + 2 + 1 + o["log1p"]["fp64"])
+    # landed (contract R10, division-free): F2I, 2 IADD, gather (LDG + address), X = DMUL, D = DADD,
+    # accept: u01 + 3 DMUL + DSETP, log1p
+    land_u = unit(1 + 2 + 2 + 1 + 1 + o["u01"]["inst"] + 3 + 1 + o["log1p"]["inst"],
+                  1 + 1 + 1 + o["u01"]["fp64"] + 3 + 1 + o["log1p"]["fp64"])
+    # ECM landed: + gathers y, log y; z, t, 1-t, Dp; accept 3 DMUL + DSETP; dq = DADD; z*iomT; log1p
+    land_e = unit(1 + 2 + 6 + 4 + o["u01"]["inst"] + 3 + 1 + 1 + 1 + o["log1p"]["inst"],
+                  1 + 4 + o["u01"]["fp64"] + 3 + 1 + 1 + 1 + o["log1p"]["fp64"])
     acc_u = unit(6, 0)
-    acc_e = unit(6 + 2 + o["u01"]["inst"] + 2 * o["log"]["inst"] + o["ddiv"]["inst"] + 4,
-                 o["u01"]["fp64"] + 2 * o["log"]["fp64"] + o["ddiv"]["fp64"] + 3)
+    # ECM accepted: log(u01) + DADD (log y_u + log y_v) + div + floor + F2I + saturation test + weight store
+    acc_e = unit(6 + 2 + o["u01"]["inst"] + o["log"]["inst"] + 1 + o["ddiv"]["inst"] + 4,
+                 o["u01"]["fp64"] + o["log"]["fp64"] + 1 + o["ddiv"]["fp64"] + 3)
     out = {
         "source": f"scripts/microbench_ops.cu under ncu ({path}); B200, CUDA 12.9",
         "impl": impl,
