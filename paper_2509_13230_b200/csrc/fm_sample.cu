@@ -52,250 +52,272 @@ __device__ __forceinline__ void load_logtab()
     __syncthreads();
 }
 
-template <int kModel, int kMinBlocks>
+// kC independent chains (lane-chunk tasks) per thread, interleaved for instruction-level
+// parallelism: with one chain a warp spends most stalls waiting on fixed-latency fp64 / IMAD
+// dependency chains (ncu: "wait"); two independent chains per thread let the scheduler overlap
+// them and amortise the loop / task-management instructions over two draws.
+template <int kModel, int kMinBlocks, int kC>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
-    __shared__ SegRec s_next[kThreads];
+    extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
+    constexpr int kRecBytes = kModel == FM_ECM ? 96 : 64;  // bytes of SegRec the model reads
     load_logtab();
     const SmemLogTab T;
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
 
-    // ---- task (lane-chunk) state ----
-    int64_t task = -1, slot = 0, sp = -1;
-    // warp batch of task ids [bpos, bend); lane 0 holds the start of the next batch
+    // ---- warp batch of task ids [bpos, bend); lane 0 holds the start of the next batch ----
     unsigned long long next_batch = 0;
     if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
     int64_t bpos = 0, bend = 0;
-    int32_t g = 0, g_end = 0, cnt = 0, cap = 0;
-    uint32_t s_abs = 0;
     bool warp_done = false;
-    // ---- current segment ----
-    bool act = false;
-    int32_t u = 0, b = 0, cur = 0, id_u = 0;
-    uint32_t sg = 0, d = 0;
-    double xq = 0.0, dq = 1.0, h = 0.0, ku = 0.0, yu = 0.0, lyu = 0.0, omT = 1.0, iomT = 1.0, E = 0.0;
-    uint32_t wacc = 0, wwt = 0;
-    // ---- counters ----
+    // ---- per-chain task state ----
+    int64_t task[kC], slot[kC], sp[kC];
+    int32_t g[kC], g_end[kC], cnt[kC], cap[kC];
+    uint32_t s_abs[kC];
+    // ---- per-chain segment state ----
+    bool act[kC];
+    int32_t u[kC], b[kC], cur[kC], id_u[kC];
+    uint32_t sg[kC], d[kC], wacc[kC], wwt[kC];
+    double xq[kC], dq[kC], h[kC], ku[kC], E[kC], yu[kC], lyu[kC], omT[kC], iomT[kC];
+#pragma unroll
+    for (int c = 0; c < kC; c++) {
+        task[c] = -1; slot[c] = 0; sp[c] = -1;
+        g[c] = g_end[c] = cnt[c] = cap[c] = 0;
+        s_abs[c] = 0;
+        act[c] = false;
+        u[c] = b[c] = cur[c] = id_u[c] = 0;
+        sg[c] = d[c] = wacc[c] = wwt[c] = 0;
+        xq[c] = 0.0; dq[c] = 1.0; h[c] = 0.0; ku[c] = 0.0; E[c] = 0.0;
+        yu[c] = 0.0; lyu[c] = 0.0; omT[c] = 1.0; iomT[c] = 1.0;
+    }
     uint32_t n_draw = 0, n_land = 0, n_acc = 0;
     bool wsat = false;
 
-    // segment g of the current task becomes current.  The record of segment g+1 is prefetched
-    // into this thread's shared-memory slot with cp.async (no registers held), so a restart
-    // after a terminal draw reads shared memory instead of waiting on a global load.
-    SegRec *my_next = &s_next[threadIdx.x];
-    const uint32_t my_next_sa = (uint32_t)__cvta_generic_to_shared(my_next);
-    auto start_seg = [&](bool prefetched) {
-        const SegRec *r = prefetched ? my_next : A.rec + g;
+    // segment g[c] of chain c's task becomes current (64/96-byte record; the record of the next
+    // segment is prefetched into this chain's shared-memory slot with cp.async)
+    auto start_seg = [&](const int c, const bool prefetched) {
+        SegRec *my_next = reinterpret_cast<SegRec *>(s_dyn + (threadIdx.x * kC + c) * kRecBytes);
+        const SegRec *r = prefetched ? my_next : A.rec + g[c];
         if (prefetched) asm volatile("cp.async.wait_all;\n" ::: "memory");
         const int4 p0 = *reinterpret_cast<const int4 *>(r);
         const double2 p1 = *reinterpret_cast<const double2 *>(&r->h0);
         const double2 p2 = *reinterpret_cast<const double2 *>(&r->d0);
         const int4 p3 = *reinterpret_cast<const int4 *>(&r->id_u);
-        u = p0.x;
-        cur = p0.y - 1;  // virtual previous position a-1 (R3)
-        b = p0.z;
-        sg = (uint32_t)p0.w;
-        h = p1.x;
-        xq = p1.y;
-        dq = p2.x;
-        ku = p2.y;
-        id_u = p3.x;
+        u[c] = p0.x;
+        cur[c] = p0.y - 1;  // virtual previous position a-1 (R3)
+        b[c] = p0.z;
+        sg[c] = (uint32_t)p0.w;
+        h[c] = p1.x;
+        xq[c] = p1.y;
+        dq[c] = p2.x;
+        ku[c] = p2.y;
+        id_u[c] = p3.x;
         if (kModel == FM_ECM) {
             const double2 p4 = *reinterpret_cast<const double2 *>(&r->yu);
             const double2 p5 = *reinterpret_cast<const double2 *>(&r->omT);
-            yu = p4.x;
-            lyu = p4.y;
-            omT = p5.x;
-            iomT = p5.y;
+            yu[c] = p4.x;
+            lyu[c] = p4.y;
+            omT[c] = p5.x;
+            iomT[c] = p5.y;
         }
-        d = 0;
-        g++;
-        act = true;
-        if (g < g_end) {
-            const char *src = reinterpret_cast<const char *>(A.rec + g);
+        d[c] = 0;
+        g[c]++;
+        act[c] = true;
+        if (g[c] < g_end[c]) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(my_next);
+            const char *src = reinterpret_cast<const char *>(A.rec + g[c]);
             constexpr int parts = kModel == FM_ECM ? 6 : 4;
 #pragma unroll
             for (int k = 0; k < parts; k++)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(my_next_sa + 16 * k),
-                             "l"(src + 16 * k)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * k), "l"(src + 16 * k)
                              : "memory");
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
     };
-    auto draw_words = [&]() {  // E and the accept/weight words of draw d (R1, R2)
+    // E and the accept/weight words of chain c's draw d[c] (R1, R2)
+    auto draw_words = [&](const int c) {
         uint32_t ws;
         if (kModel == FM_UBCM) {
-            const uint4 W = philox4x32_10(make_uint4(d >> 1, sg, (uint32_t)u, s_abs), A.key);
-            ws = (d & 1) ? W.z : W.x;
-            wacc = (d & 1) ? W.w : W.y;
+            const uint4 W = philox4x32_10(make_uint4(d[c] >> 1, sg[c], (uint32_t)u[c], s_abs[c]), A.key);
+            ws = (d[c] & 1) ? W.z : W.x;
+            wacc[c] = (d[c] & 1) ? W.w : W.y;
         } else {
-            const uint4 W = philox4x32_10(make_uint4(d, sg, (uint32_t)u, s_abs), A.key);
+            const uint4 W = philox4x32_10(make_uint4(d[c], sg[c], (uint32_t)u[c], s_abs[c]), A.key);
             ws = W.x;
-            wacc = W.y;
-            wwt = W.z;
+            wacc[c] = W.y;
+            wwt[c] = W.z;
         }
-        E = -fm_log(u01(ws), T);
+        return -fm_log(u01(ws), T);
     };
 
     for (;;) {
-        // ---- 1. task management (lanes whose task has no segment left) ----
-        // Tasks come in warp batches of kBatch consecutive ids from the global queue; the next
-        // batch is requested (by lane 0) as soon as the current one is opened, so the atomic's
-        // latency is never waited for.
-        const bool needc = !act;
-        if (needc && task >= 0) {
-            if (!A.rerun_base) {
-                A.counts[task] = cnt;
-                A.spill_off[task] = sp;
+        // ---- 1. task management: chains whose task has no segment left take the next task ids
+        //      of the warp's batch (the next batch is requested as soon as one is opened) ----
+        bool fresh[kC];
+#pragma unroll
+        for (int c = 0; c < kC; c++) {
+            fresh[c] = false;
+            const bool needc = !act[c];
+            if (needc && task[c] >= 0) {
+                if (!A.rerun_base) {
+                    A.counts[task[c]] = cnt[c];
+                    A.spill_off[task[c]] = sp[c];
+                }
+                task[c] = -1;
             }
-            task = -1;
-        }
-        const uint32_t nc = __ballot_sync(0xffffffffu, needc && !warp_done);
-        bool fresh = false;
-        if (nc) {
-            const int k = __popc(nc), rank = __popc(nc & lt);
-            const int64_t avail = bend - bpos;
-            int64_t my;
-            if (k <= avail) {
-                my = bpos + rank;
-                bpos += k;
-            } else {
-                const int64_t nb = (int64_t)__shfl_sync(0xffffffffu, next_batch, 0);
-                my = rank < avail ? bpos + rank : nb + (rank - avail);
-                bpos = nb + (k - avail);
-                bend = nb + kBatch;
-                if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
-            }
-            if (needc && !warp_done && my < A.n_tasks) {
-                const int64_t t = A.task_list ? A.task_list[my] : my;
-                const int64_t s = t / A.n_chunks, c = t - s * A.n_chunks;
-                task = t;
-                g = (int32_t)A.chunk_seg[c];
-                g_end = (int32_t)A.chunk_seg[c + 1];
-                if (A.rerun_base) {
-                    slot = A.rerun_base[t];
-                    cap = INT32_MAX;
+            const uint32_t nc = __ballot_sync(0xffffffffu, needc && !warp_done);
+            if (nc) {
+                const int k = __popc(nc), rank = __popc(nc & lt);
+                const int64_t avail = bend - bpos;
+                int64_t my;
+                if (k <= avail) {
+                    my = bpos + rank;
+                    bpos += k;
                 } else {
-                    slot = s * A.cap_per_sample + A.chunk_cap[c];
-                    cap = (int32_t)(A.chunk_cap[c + 1] - A.chunk_cap[c]);
+                    const int64_t nb = (int64_t)__shfl_sync(0xffffffffu, next_batch, 0);
+                    my = rank < avail ? bpos + rank : nb + (rank - avail);
+                    bpos = nb + (k - avail);
+                    bend = nb + kBatch;
+                    if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
                 }
-                s_abs = A.first_sample + (uint32_t)s;
-                cnt = 0;
-                sp = -1;
-                if (g < g_end) {
-                    start_seg(false);
-                    fresh = true;
+                if (needc && !warp_done && my < A.n_tasks) {
+                    const int64_t t = A.task_list ? A.task_list[my] : my;
+                    const int64_t s = t / A.n_chunks, ch = t - s * A.n_chunks;
+                    task[c] = t;
+                    g[c] = (int32_t)A.chunk_seg[ch];
+                    g_end[c] = (int32_t)A.chunk_seg[ch + 1];
+                    if (A.rerun_base) {
+                        slot[c] = A.rerun_base[t];
+                        cap[c] = INT32_MAX;
+                    } else {
+                        slot[c] = s * A.cap_per_sample + A.chunk_cap[ch];
+                        cap[c] = (int32_t)(A.chunk_cap[ch + 1] - A.chunk_cap[ch]);
+                    }
+                    s_abs[c] = A.first_sample + (uint32_t)s;
+                    cnt[c] = 0;
+                    sp[c] = -1;
+                    if (g[c] < g_end[c]) {
+                        start_seg(c, false);
+                        fresh[c] = true;
+                    }
                 }
+                if (bpos >= A.n_tasks) warp_done = true;
             }
-            if (bpos >= A.n_tasks) warp_done = true;
         }
-        if (!__any_sync(0xffffffffu, act)) {
+        bool any_act = false;
+#pragma unroll
+        for (int c = 0; c < kC; c++) any_act = any_act || act[c];
+        if (!__any_sync(0xffffffffu, any_act)) {
             if (warp_done) break;
             continue;
         }
         // ---- 2. first draw of a freshly fetched task ----
-        if (fresh) draw_words();
+#pragma unroll
+        for (int c = 0; c < kC; c++)
+            if (fresh[c]) E[c] = draw_words(c);
 
-        // ---- 3. consume one draw ----
-        bool landed = false;
-        uint32_t w_land = 0, w_wt = 0;
-        double kv = 0.0, yv = 0.0, lyv = 0.0;
-        int32_t id_v = 0;
-        if (act) {
-            n_draw++;
-            const double R = __ddiv_rn(E, h);
-            if (!(R < (double)(b - 1 - cur))) {  // terminal draw (R5)
-                if (g < g_end) start_seg(true);
-                else act = false;
-            } else {
-                cur = cur + 1 + (int32_t)R;  // R >= 0: truncation == floor
-                kv = A.kappa_s[cur];
-                if (kModel == FM_ECM) {
-                    yv = A.y_s[cur];
-                    lyv = A.ly_s[cur];
+        // ---- 3. consume one draw per chain ----
+        bool landed[kC];
+        uint32_t w_land[kC], w_wt[kC];
+        double kv[kC], yv[kC], lyv[kC];
+        int32_t id_v[kC];
+#pragma unroll
+        for (int c = 0; c < kC; c++) {
+            landed[c] = false;
+            w_land[c] = w_wt[c] = 0;
+            kv[c] = yv[c] = lyv[c] = 0.0;
+            id_v[c] = 0;
+            if (act[c]) {
+                n_draw++;
+                const double R = __ddiv_rn(E[c], h[c]);
+                if (!(R < (double)(b[c] - 1 - cur[c]))) {  // terminal draw (R5)
+                    if (g[c] < g_end[c]) start_seg(c, true);
+                    else act[c] = false;
+                } else {
+                    cur[c] = cur[c] + 1 + (int32_t)R;  // R >= 0: truncation == floor
+                    kv[c] = A.kappa_s[cur[c]];
+                    if (kModel == FM_ECM) {
+                        yv[c] = A.y_s[cur[c]];
+                        lyv[c] = A.ly_s[cur[c]];
+                    }
+                    id_v[c] = A.perm[cur[c]];  // issued early; needed only if accepted
+                    landed[c] = true;
+                    w_land[c] = wacc[c];
+                    w_wt[c] = wwt[c];
+                    d[c]++;
+                    n_land++;
                 }
-                id_v = A.perm[cur];  // issued early; needed only if accepted
-                landed = true;
-                w_land = wacc;
-                w_wt = wwt;
-                d++;
-                n_land++;
             }
         }
-        // ---- 4+5. one straight-line block for every active lane: RNG + E of the next draw
-        //      (overlaps the k[cur] gather) interleaved with the p/q test of the landed candidate
-        //      (lanes that restarted a segment evaluate a dummy X = 1 and keep their h0, q0) ----
-        bool acc = false;
-        int32_t w = 1;
-        if (act) {
-            uint32_t ws;
-            if (kModel == FM_UBCM) {
-                const uint4 W = philox4x32_10(make_uint4(d >> 1, sg, (uint32_t)u, s_abs), A.key);
-                ws = (d & 1) ? W.z : W.x;
-                wacc = (d & 1) ? W.w : W.y;
-            } else {
-                const uint4 W = philox4x32_10(make_uint4(d, sg, (uint32_t)u, s_abs), A.key);
-                ws = W.x;
-                wacc = W.y;
-                wwt = W.z;
-            }
-            const double Enew = -fm_log(u01(ws), T);
-            if (kModel == FM_UBCM) {
+        // ---- 4+5. per chain, one straight-line block: RNG + E of the next draw (overlaps the
+        //      k[cur] gather) and the p/q test of the landed candidate (restarted chains
+        //      evaluate a dummy X = 1 and keep their h0, x0, d0) ----
+        bool acc[kC];
+        int32_t w[kC];
+#pragma unroll
+        for (int c = 0; c < kC; c++) {
+            acc[c] = false;
+            w[c] = 1;
+            if (act[c]) {
+                const double Enew = draw_words(c);
                 // (kv + 0*Enew) orders the use of the gathered kv after the RNG/log work above,
                 // so the gather latency hides behind it; exact since Enew is finite and kv >= 0
-                const double kvd = __dadd_rn(kv, __dmul_rn(Enew, 0.0));
-                const double X = landed ? __dmul_rn(ku, kvd) : 1.0;  // dummy for restarted lanes
-                const double D = __dadd_rn(1.0, X);
-                const double hn = fm_log1p(X, T);
-                if (landed) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
-                    acc = __dmul_rn(__dmul_rn(u01(w_land), xq), D) < __dmul_rn(X, dq);
-                    xq = X;
-                    dq = D;
-                    h = hn;
-                }
-            } else {
-                const double kvd = __dadd_rn(kv, __dmul_rn(Enew, 0.0));  // see UBCM
-                const double z = landed ? __dmul_rn(ku, kvd) : 1.0;  // dummy for restarted lanes
-                const double t = __dmul_rn(yu, yv);
-                const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
-                const double hn = fm_log1p(__dmul_rn(z, iomT), T);
-                if (landed) {
-                    acc = __dmul_rn(__dmul_rn(u01(w_land), xq), Dp) < __dmul_rn(z, dq);
-                    xq = z;
-                    dq = __dadd_rn(omT, z);
-                    h = hn;
-                    if (acc) {  // Eq. 5 weight, log t = log y_u + log y_v (R8)
-                        const double lu = fm_log(u01(w_wt), T);
-                        const double G = floor(__ddiv_rn(lu, __dadd_rn(lyu, lyv)));
-                        if (G <= 2147483646.0) {
-                            w = 1 + (int32_t)G;
-                        } else {
-                            w = INT32_MAX;
-                            wsat = true;
+                const double kvd = __dadd_rn(kv[c], __dmul_rn(Enew, 0.0));
+                if (kModel == FM_UBCM) {
+                    const double X = landed[c] ? __dmul_rn(ku[c], kvd) : 1.0;
+                    const double D = __dadd_rn(1.0, X);
+                    const double hn = fm_log1p(X, T);
+                    if (landed[c]) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
+                        acc[c] = __dmul_rn(__dmul_rn(u01(w_land[c]), xq[c]), D) < __dmul_rn(X, dq[c]);
+                        xq[c] = X;
+                        dq[c] = D;
+                        h[c] = hn;
+                    }
+                } else {
+                    const double z = landed[c] ? __dmul_rn(ku[c], kvd) : 1.0;
+                    const double t = __dmul_rn(yu[c], yv[c]);
+                    const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
+                    const double hn = fm_log1p(__dmul_rn(z, iomT[c]), T);
+                    if (landed[c]) {
+                        acc[c] = __dmul_rn(__dmul_rn(u01(w_land[c]), xq[c]), Dp) < __dmul_rn(z, dq[c]);
+                        xq[c] = z;
+                        dq[c] = __dadd_rn(omT[c], z);
+                        h[c] = hn;
+                        if (acc[c]) {  // Eq. 5 weight, log t = log y_u + log y_v (R8)
+                            const double lu = fm_log(u01(w_wt[c]), T);
+                            const double G = floor(__ddiv_rn(lu, __dadd_rn(lyu[c], lyv[c])));
+                            if (G <= 2147483646.0) {
+                                w[c] = 1 + (int32_t)G;
+                            } else {
+                                w[c] = INT32_MAX;
+                                wsat = true;
+                            }
                         }
                     }
                 }
+                E[c] = Enew;
             }
-            E = Enew;
         }
-        if (landed) {
-            if (acc) {
-                const int2 ev = make_int2(min(id_u, id_v), max(id_u, id_v));
-                if (cnt < cap) {
-                    A.edges[slot + cnt] = ev;
-                    if (kModel == FM_ECM) A.weights[slot + cnt] = w;
-                } else if (!A.rerun_base && cnt < 2 * cap) {  // spill: one extra region of `cap` edges
-                    if (sp == -1) {
-                        const unsigned long long o = atomicAdd(A.spill_counter, (unsigned long long)cap);
-                        sp = (int64_t)(o + cap) <= A.spill_cap ? (int64_t)o : -2;
+        // ---- 6. append accepted edges to the tasks' slots, in draw order ----
+#pragma unroll
+        for (int c = 0; c < kC; c++) {
+            if (acc[c]) {
+                const int2 ev = make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
+                if (cnt[c] < cap[c]) {
+                    A.edges[slot[c] + cnt[c]] = ev;
+                    if (kModel == FM_ECM) A.weights[slot[c] + cnt[c]] = w[c];
+                } else if (!A.rerun_base && cnt[c] < 2 * cap[c]) {  // spill: one extra region of `cap`
+                    if (sp[c] == -1) {
+                        const unsigned long long o = atomicAdd(A.spill_counter, (unsigned long long)cap[c]);
+                        sp[c] = (int64_t)(o + cap[c]) <= A.spill_cap ? (int64_t)o : -2;
                     }
-                    if (sp >= 0) {
-                        A.spill_e[sp + cnt - cap] = ev;
-                        if (kModel == FM_ECM) A.spill_w[sp + cnt - cap] = w;
+                    if (sp[c] >= 0) {
+                        A.spill_e[sp[c] + cnt[c] - cap[c]] = ev;
+                        if (kModel == FM_ECM) A.spill_w[sp[c] + cnt[c] - cap[c]] = w[c];
                     }
                 }
-                cnt++;
+                cnt[c]++;
                 n_acc++;
             }
         }
@@ -470,29 +492,41 @@ cudaError_t ensure_log_table(cudaStream_t st)
 
 // the sampler is instantiated for several register budgets (min resident blocks per SM);
 // FM_SAMPLE_MINB selects one at run time (tuning), default per model
-template <int kModel, int kMinB>
+template <int kModel, int kMinB, int kC>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB>, kThreads, 0);
+    const size_t dyn = (size_t)kThreads * kC * (kModel == FM_ECM ? 96 : 64);
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_sample<kModel, kMinB, kC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        attr_set = true;
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC>, kThreads, dyn);
     int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
-    const int64_t need = (a.n_tasks + kThreads - 1) / kThreads;  // at most one task per lane at start
+    const int64_t need = (a.n_tasks + kThreads * kC - 1) / (kThreads * kC);  // <= one task per chain at start
     if (need < blocks) blocks = need;
     count_launch();
-    k_sample<kModel, kMinB><<<(unsigned)blocks, kThreads, 0, st>>>(a);
+    k_sample<kModel, kMinB, kC><<<(unsigned)blocks, kThreads, dyn, st>>>(a);
     return cudaGetLastError();
 }
 
 template <int kModel>
-static cudaError_t launch_sample_m(int minb, const SampleArgs &a, cudaStream_t st)
+static cudaError_t launch_sample_m(int chains, int minb, const SampleArgs &a, cudaStream_t st)
 {
+    if (chains == 2) {
+        switch (minb) {
+        case 1: return launch_sample_t<kModel, 1, 2>(a, st);
+        case 3: return launch_sample_t<kModel, 3, 2>(a, st);
+        default: return launch_sample_t<kModel, 2, 2>(a, st);
+        }
+    }
     switch (minb) {
-    case 1: return launch_sample_t<kModel, 1>(a, st);
-    case 2: return launch_sample_t<kModel, 2>(a, st);
-    case 4: return launch_sample_t<kModel, 4>(a, st);
-    default: return launch_sample_t<kModel, 3>(a, st);
+    case 2: return launch_sample_t<kModel, 2, 1>(a, st);
+    case 4: return launch_sample_t<kModel, 4, 1>(a, st);
+    default: return launch_sample_t<kModel, 3, 1>(a, st);
     }
 }
 
@@ -508,8 +542,11 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
         if (e != cudaSuccess) return e;
     }
     const char *ev = getenv("FM_SAMPLE_MINB");
-    const int minb = ev && *ev ? atoi(ev) : (model == FM_UBCM ? 3 : 2);
-    return model == FM_UBCM ? launch_sample_m<FM_UBCM>(minb, a, st) : launch_sample_m<FM_ECM>(minb, a, st);
+    const char *ec = getenv("FM_SAMPLE_CHAINS");
+    const int chains = ec && *ec ? atoi(ec) : 1;
+    const int minb = ev && *ev ? atoi(ev) : (chains == 2 ? 2 : (model == FM_UBCM ? 3 : 2));
+    return model == FM_UBCM ? launch_sample_m<FM_UBCM>(chains, minb, a, st)
+                            : launch_sample_m<FM_ECM>(chains, minb, a, st);
 }
 
 cudaError_t launch_overflow(int64_t n_tasks, int64_t n_chunks, const int64_t *chunk_cap, const int64_t *counts,
