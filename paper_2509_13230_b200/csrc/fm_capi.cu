@@ -162,6 +162,7 @@ void plan_release(Plan *p)
     cudaFree(p->rec);
     cudaFree(p->chunk_seg);
     cudaFree(p->chunk_cap);
+    cudaFree(p->dev_flags);
     p->magic = 0;
     delete p;
 }
@@ -241,10 +242,8 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     count_launch();
     k_validate_key<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, xd, yd, ka, ia, sc, hist);
     CK(cudaGetLastError(), "k_validate_key");
-    CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
-    CK(cudaStreamSynchronize(st), "sync (validate)");
-    if (h_sc.flags & kErrInvalid)
-        return fail(FM_ERR_INVALID, "invalid fitness: x must be finite >= 0, y in [0,1), kappa_max^2 finite");
+    // (no sync here: the validation flag is read with the segment count below; the kernels in
+    //  between are harmless on invalid input)
 
     Plan *p = new Plan();
     memset(p, 0, sizeof(Plan));
@@ -264,7 +263,8 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(tmp.get((char **)&work, tmp_bytes), "alloc sort tmp");
     uint64_t *skeys;
     int32_t *perm;
-    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, (uint64_t)(h_sc.key_or ^ h_sc.key_and), hist, &skeys, &perm, work,
+    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, ~0ull /* all 8 digit passes; a constant digit is a stable copy */,
+                          hist, &skeys, &perm, work,
                           tmp_bytes, st),
        "radix sort");
     tmp.release(perm);
@@ -303,6 +303,8 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
     CK(cudaMemcpyAsync(&n_seg, row_m + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "read n_seg");
     CK(cudaStreamSynchronize(st), "sync (rows)");
+    if (h_sc.flags & kErrInvalid)
+        return fail(FM_ERR_INVALID, "invalid fitness: x must be finite >= 0, y in [0,1), kappa_max^4 finite");
     p->F = h_sc.F;
     p->n_seg = n_seg;
     p->wmax = h_sc.wmax;
@@ -360,10 +362,11 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
         p->cap_per_sample = cap_override * p->n_chunks;
     }
 
-    CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
+    // the cut invariant (kErrState, impossible for S >= 8) is checked lazily by fm_sample_*: the
+    // plan keeps the flag word on the device and returns without a third synchronisation
+    CK(cudaMallocAsync((void **)&p->dev_flags, sizeof(unsigned int), st), "alloc flags");
+    CK(cudaMemcpyAsync(p->dev_flags, &sc->flags, sizeof(unsigned int), cudaMemcpyDeviceToDevice, st), "copy flags");
     timer.end(st);
-    CK(cudaStreamSynchronize(st), "sync (plan)");
-    if (h_sc.flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
 
     guard.p = nullptr;
     {
@@ -482,7 +485,11 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
            "read offsets");
         CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+        unsigned int plan_flags = 0;
+        CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
+           "read plan flags");
         CK(cudaStreamSynchronize(st), "sync (sample)");
+        if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
         const int64_t total = offsets_h[n_samples];
         CK(cudaMallocAsync(&own->edges, sizeof(int2) * std::max<int64_t>(total, 1), st), "alloc edges");
         if (model == FM_ECM)

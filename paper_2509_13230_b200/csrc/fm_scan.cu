@@ -173,23 +173,32 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64
     }
     uint64_t tot;
     const uint64_t exc = block_exclusive<SumU64>(acc, &tot);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
+        const int lane = threadIdx.x;
         uint64_t prefix = 0;
         if (tile == 0) {
-            *(volatile uint64_t *)(status) = kFlagInc | tot;
+            if (lane == 0) *(volatile uint64_t *)(status) = kFlagInc | tot;
         } else {
-            *(volatile uint64_t *)(status + tile) = kFlagAgg | tot;
-            for (int64_t j = tile - 1; j >= 0; j--) {
-                uint64_t w;
-                do {
-                    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(w) : "l"(status + j));
-                } while ((w & ~kValMask) == 0);
-                prefix += w & kValMask;
-                if ((w & ~kValMask) == kFlagInc) break;
+            if (lane == 0) *(volatile uint64_t *)(status + tile) = kFlagAgg | tot;
+            for (int64_t j_end = tile;; j_end -= 32) {
+                const int64_t j = j_end - 1 - lane;  // lane 0 = nearest predecessor
+                uint64_t v = kFlagInc;               // before tile 0: an inclusive prefix of 0
+                if (j >= 0) {
+                    do {
+                        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(status + j));
+                    } while ((v & ~kValMask) == 0);
+                }
+                const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
+                const int first = inc ? __ffs(inc) - 1 : 32;
+                uint64_t c = lane <= first ? (v & kValMask) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                prefix += c;
+                if (inc) break;
             }
-            *(volatile uint64_t *)(status + tile) = kFlagInc | (prefix + tot);
+            if (lane == 0) *(volatile uint64_t *)(status + tile) = kFlagInc | (prefix + tot);
         }
-        s_prefix = prefix;
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
     uint64_t pre = s_prefix + exc;

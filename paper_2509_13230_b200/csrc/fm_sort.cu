@@ -91,13 +91,20 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
             *(volatile uint64_t *)my = kFlagInc | cnt;
         } else {
             *(volatile uint64_t *)my = kFlagAgg | cnt;
-            for (int64_t j = tile - 1; j >= 0; j--) {
-                uint64_t v;
-                do {
-                    v = ld_volatile_u64(status + j * kRadix + d);
-                } while ((v & ~kValMask) == 0);
-                prefix += v & kValMask;
-                if ((v & ~kValMask) == kFlagInc) break;
+            // look back 8 predecessor tiles at a time (independent loads in flight)
+            for (int64_t j = tile - 1; j >= 0; j -= 8) {
+                uint64_t v[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) v[k] = j - k >= 0 ? ld_volatile_u64(status + (j - k) * kRadix + d) : kFlagInc;
+                bool done = false;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    if (done) break;
+                    while ((v[k] & ~kValMask) == 0) v[k] = ld_volatile_u64(status + (j - k) * kRadix + d);
+                    prefix += v[k] & kValMask;
+                    done = (v[k] & ~kValMask) == kFlagInc;
+                }
+                if (done) break;
             }
             *(volatile uint64_t *)my = kFlagInc | (prefix + cnt);
         }
