@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
     };
-    // E and the accept/weight words of chain c's draw d[c] (R1, R2)
-    auto draw_words = [&](const int c) {
+    // u01 of the skip word, and the accept/weight words, of chain c's draw d[c] (R1, R2)
+    auto draw_u = [&](const int c) {
         uint32_t ws;
         if (kModel == FM_UBCM) {
             const uint4 W = philox4x32_10(make_uint4(d[c] >> 1, sg[c], (uint32_t)u[c], s_abs[c]), A.key);
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             wacc[c] = W.y;
             wwt[c] = W.z;
         }
-        return -fm_log(u01(ws), T);
+        return u01(ws);
     };
 
     for (;;) {
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         // ---- 2. first draw of a freshly fetched task ----
 #pragma unroll
         for (int c = 0; c < kC; c++)
-            if (fresh[c]) E[c] = draw_words(c);
+            if (fresh[c]) E[c] = -fm_log(draw_u(c), T);
 
         // ---- 3. consume one draw per chain ----
         bool landed[kC];
@@ -260,10 +260,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             acc[c] = false;
             w[c] = 1;
             if (act[c]) {
-                const double Enew = draw_words(c);
-                // (kv + 0*Enew) orders the use of the gathered kv after the RNG/log work above,
-                // so the gather latency hides behind it; exact since Enew is finite and kv >= 0
-                const double kvd = __dadd_rn(kv[c], __dmul_rn(Enew, 0.0));
+                const double us = draw_u(c);
+                // (kv + 0*us) orders the use of the gathered kv after the Philox rounds above, so
+                // the gather latency hides behind them while the two logarithms below (E of the
+                // next draw, log1p of this candidate) stay independent; exact since us in (0,1)
+                const double kvd = __dadd_rn(kv[c], __dmul_rn(us, 0.0));
+                const double Enew = -fm_log(us, T);
                 if (kModel == FM_UBCM) {
                     const double X = landed[c] ? __dmul_rn(ku[c], kvd) : 1.0;
                     const double D = __dadd_rn(1.0, X);
