@@ -114,7 +114,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ roofline
-def roofline(model: str, counters: dict, kernel_ms: float, launches: int):
+def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: int = 2):
     """Roofline of the dominant kernel k_sample.
 
     Compute term: algorithmic warp-instructions of the chain (op list of DESIGN 7.1, per-op
@@ -148,8 +148,16 @@ def roofline(model: str, counters: dict, kernel_ms: float, launches: int):
         ach, peak, unit = fp64_l / t / 1e9, fp64_peak / 1e9, "G fp64 warp-inst/s"
     else:
         ach, peak, unit = inst_l / t / 1e9, issue_peak / 1e9, "G warp-inst/s"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath)).get("k_sample", {}).get(f"{model}_cfg{cfg}")
+        if tr:
+            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
     return {"bound": "alu" if bound != "hbm" else "hbm", "resource": bound, "achieved": ach, "peak": peak,
-            "unit": unit, "frac": ach / peak, "traffic": None, "kernel": "k_sample",
+            "unit": unit, "frac": ach / peak, "traffic": traffic,
+            "traffic_note": "dram read+write bytes per launch from one ncu --set full capture (profiles/traffic.json)",
+            "kernel": "k_sample",
             "kernel_ms_per_launch": t * 1e3, "t_roof_ms": max(t_issue, t_fp64, t_mem) * 1e3,
             "terms_ms": {"issue": t_issue * 1e3, "fp64": t_fp64 * 1e3, "hbm": t_mem * 1e3},
             "alg_warp_inst_per_launch": inst_l, "alg_fp64_warp_inst_per_launch": fp64_l,
@@ -312,7 +320,7 @@ def run_own(args):
             dist.destroy_process_group()
         return
 
-    rf = roofline(w.model, tot, tim["sample_ms"], max(1, tim["sample_launches"]))
+    rf = roofline(w.model, tot, tim["sample_ms"], max(1, tim["sample_launches"]), cfg=args.config)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         c = cpu_oracle_run(w, x, y, args.seg_target, args.cpu_seconds)
