@@ -66,17 +66,23 @@ int64_t fmo_skip(uint32_t k, double h)
 /* ------------------------------------------------------------------------------------------ */
 struct fmo_plan {
     int model;
-    int64_t n, S;
+    int kind;         /* FMO_UNDIRECTED, FMO_BIPARTITE, FMO_DIRECTED            */
+    int64_t n, nc, S; /* n rows (the + set / out-nodes), nc candidates (the - set / in-nodes)   */
     int F;
+    /* rows, in rank order of their own sort (P:L133 (i)) */
     int32_t *perm;    /* perm[r] = original id of sorted rank r                          */
     double *kappa_s;  /* sort key in rank order: x (UBCM) or x*y (ECM)                   */
     double *y_s;      /* ECM: y in rank order                                            */
-    double *ymax;     /* ECM: ymax[t] = max_{w>=t} y_s[w], ymax[n] = 0 (beta_min, R6)    */
-    uint64_t *P;      /* fixed-point prefix of kappa_s, n+1 entries (planner, 3.4)       */
+    double *ly_s;     /* ECM: log(y) in rank order (weights, reading R8)                 */
+    /* candidates (undirected: the same arrays as the rows) */
+    int32_t *cperm;
+    double *ckappa, *cy, *cly;
+    double *ymax;     /* ECM: ymax[t] = max_{w>=t} cy[w], ymax[nc] = 0 (beta_min, R6)    */
+    uint64_t *P;      /* fixed-point prefix of ckappa, nc+1 entries (planner, 3.4)       */
+    int32_t *excl;    /* directed: excl[u] = candidate rank of row u's own node (no self loops) */
     int64_t *row_seg; /* first segment of each row, n+1 entries                          */
     int64_t nseg;
     int32_t *seg_u, *seg_a, *seg_b, *seg_sigma;
-    double *ly_s;     /* ECM: log(y) in rank order (weights, reading R8')                 */
     double *seg_h0, *seg_x0, *seg_d0, *seg_omT, *seg_iomT;
 };
 
@@ -103,12 +109,15 @@ static int ceil_log2_i64(int64_t n)
     return L;
 }
 
-/* W_i(v): integer estimate (units 2^-G draws) of the draws a row-i chain makes over candidates
- * [i+1, v); saturated part counts 1 per candidate, the rest r_i * sum kappa. */
-static int64_t plan_W(const fmo_plan *p, int64_t i, double r, int64_t sat, int64_t v)
+/* first candidate of row u: undirected j > i, bipartite/directed every - node */
+static int64_t row_c0(const fmo_plan *p, int64_t u) { return p->kind == FMO_UNDIRECTED ? u + 1 : 0; }
+
+/* W_u(v): integer estimate (units 2^-G draws) of the draws a row-u chain makes over candidates
+ * [c0, v); saturated part counts 1 per candidate, the rest r_u * sum kappa. */
+static int64_t plan_W(const fmo_plan *p, int64_t c0, double r, int64_t sat, int64_t v)
 {
     int64_t vs = v < sat ? v : sat;
-    int64_t A = (vs - i - 1) * ((int64_t)1 << FMO_G);
+    int64_t A = (vs - c0) * ((int64_t)1 << FMO_G);
     int64_t B = 0;
     if (v > sat) {
         uint64_t D = p->P[v] - p->P[sat];
@@ -120,22 +129,18 @@ static int64_t plan_W(const fmo_plan *p, int64_t i, double r, int64_t sat, int64
 void fmo_plan_free(fmo_plan *p)
 {
     if (!p) return;
-    free(p->perm); free(p->kappa_s); free(p->y_s); free(p->ymax); free(p->P); free(p->row_seg);
+    if (p->cperm != p->perm) { free(p->cperm); free(p->ckappa); free(p->cy); free(p->cly); }
+    free(p->perm); free(p->kappa_s); free(p->y_s); free(p->ly_s); free(p->ymax); free(p->P); free(p->excl);
+    free(p->row_seg);
     free(p->seg_u); free(p->seg_a); free(p->seg_b); free(p->seg_sigma);
-    free(p->ly_s); free(p->seg_h0); free(p->seg_x0); free(p->seg_d0); free(p->seg_omT); free(p->seg_iomT);
+    free(p->seg_h0); free(p->seg_x0); free(p->seg_d0); free(p->seg_omT); free(p->seg_iomT);
     free(p);
 }
 
-int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int64_t seg_target,
-                    fmo_plan **out)
+/* a1 + a2 for one node set: validate, key, sort; returns the rank-order arrays */
+static int sort_set(int model, int64_t n, const double *x, const double *y, int32_t **perm, double **kappa_s,
+                    double **y_s, double **ly_s, double *kmax_out)
 {
-    *out = NULL;
-    /* ---- a1: validate + key ---- */
-    if (model != FMO_UBCM && model != FMO_ECM) return FMO_ERR_INVALID;
-    if (n < 2 || n > INT32_MAX || !x) return FMO_ERR_INVALID;
-    if (model == FMO_ECM && !y) return FMO_ERR_INVALID;
-    if (seg_target == 0) seg_target = 256;
-    if (seg_target < 8 || seg_target > ((int64_t)1 << 40)) return FMO_ERR_INVALID;
     for (int64_t i = 0; i < n; i++) {
         if (!isfinite(x[i]) || x[i] < 0.0) return FMO_ERR_INVALID;
         if (model == FMO_ECM && (!isfinite(y[i]) || y[i] < 0.0 || y[i] >= 1.0)) return FMO_ERR_INVALID;
@@ -148,45 +153,82 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
         keys[i].id = (int32_t)i;
         if (keys[i].kappa > kmax) kmax = keys[i].kappa;
     }
-    if (!isfinite((kmax * kmax) * (kmax * kmax))) { free(keys); return FMO_ERR_INVALID; } /* R10 products */
+    qsort(keys, (size_t)n, sizeof(key_t_), cmp_key);
+    *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    *kappa_s = (double *)malloc(sizeof(double) * (size_t)n);
+    if (model == FMO_ECM) {
+        *y_s = (double *)malloc(sizeof(double) * (size_t)n);
+        *ly_s = (double *)malloc(sizeof(double) * (size_t)n);
+    }
+    if (!*perm || !*kappa_s || (model == FMO_ECM && (!*y_s || !*ly_s))) { free(keys); return FMO_ERR_NOMEM; }
+    for (int64_t r = 0; r < n; r++) { (*perm)[r] = keys[r].id; (*kappa_s)[r] = keys[r].kappa; }
+    if (model == FMO_ECM)
+        for (int64_t r = 0; r < n; r++) { (*y_s)[r] = y[(*perm)[r]]; (*ly_s)[r] = log((*y_s)[r]); }
+    free(keys);
+    *kmax_out = kmax;
+    return FMO_OK;
+}
+
+int fmo_plan_create2(int model, int kind, int64_t n1, const double *x1, const double *y1, int64_t n2,
+                     const double *x2, const double *y2, int64_t seg_target, fmo_plan **out)
+{
+    *out = NULL;
+    /* ---- a1: validate ---- */
+    if (model != FMO_UBCM && model != FMO_ECM) return FMO_ERR_INVALID;
+    if (kind != FMO_UNDIRECTED && kind != FMO_BIPARTITE && kind != FMO_DIRECTED) return FMO_ERR_INVALID;
+    if (kind == FMO_UNDIRECTED) { n2 = n1; x2 = x1; y2 = y1; }
+    if (kind == FMO_DIRECTED && n1 != n2) return FMO_ERR_INVALID;
+    if (n1 < (kind == FMO_UNDIRECTED ? 2 : 1) || n1 > INT32_MAX || !x1) return FMO_ERR_INVALID;
+    if (n2 < 1 || n2 > INT32_MAX || !x2) return FMO_ERR_INVALID;
+    if (model == FMO_ECM && (!y1 || !y2)) return FMO_ERR_INVALID;
+    if (seg_target == 0) seg_target = 256;
+    if (seg_target < 8 || seg_target > ((int64_t)1 << 40)) return FMO_ERR_INVALID;
 
     fmo_plan *p = (fmo_plan *)calloc(1, sizeof(fmo_plan));
-    if (!p) { free(keys); return FMO_ERR_NOMEM; }
-    p->model = model; p->n = n; p->S = seg_target;
+    if (!p) return FMO_ERR_NOMEM;
+    p->model = model; p->kind = kind; p->n = n1; p->nc = n2; p->S = seg_target;
+    const int64_t n = n1, nc = n2;
+    /* ---- a2: sort both sets (P:L133 (i); "sorted according to ...") ---- */
+    double kmax1 = 0.0, kmax2 = 0.0;
+    int rc = sort_set(model, n1, x1, y1, &p->perm, &p->kappa_s, &p->y_s, &p->ly_s, &kmax1);
+    if (rc != FMO_OK) { fmo_plan_free(p); return rc; }
+    if (kind == FMO_UNDIRECTED) {
+        p->cperm = p->perm; p->ckappa = p->kappa_s; p->cy = p->y_s; p->cly = p->ly_s; kmax2 = kmax1;
+    } else {
+        rc = sort_set(model, n2, x2, y2, &p->cperm, &p->ckappa, &p->cy, &p->cly, &kmax2);
+        if (rc != FMO_OK) { fmo_plan_free(p); return rc; }
+    }
+    /* R10's cross products (X * D with X <= kmax1 * kmax2) stay finite */
+    if (!isfinite((kmax1 * kmax2) * (kmax1 * kmax2))) { fmo_plan_free(p); return FMO_ERR_INVALID; }
+    if (kind == FMO_DIRECTED) { /* the row node's own in-copy is not a candidate */
+        int32_t *crank = (int32_t *)malloc(sizeof(int32_t) * (size_t)nc);
+        p->excl = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+        if (!crank || !p->excl) { free(crank); fmo_plan_free(p); return FMO_ERR_NOMEM; }
+        for (int64_t r = 0; r < nc; r++) crank[p->cperm[r]] = (int32_t)r;
+        for (int64_t u = 0; u < n; u++) p->excl[u] = crank[p->perm[u]];
+        free(crank);
+    }
 
-    /* ---- a2: sort (P:L133 (i)) ---- */
-    qsort(keys, (size_t)n, sizeof(key_t_), cmp_key);
-    p->perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
-    p->kappa_s = (double *)malloc(sizeof(double) * (size_t)n);
-    if (!p->perm || !p->kappa_s) goto nomem;
-    for (int64_t r = 0; r < n; r++) { p->perm[r] = keys[r].id; p->kappa_s[r] = keys[r].kappa; }
-    free(keys); keys = NULL;
-
-    /* ---- a3: beta_min via suffix maximum of y (reading R6) ---- */
+    /* ---- a3: beta_min via suffix maximum of the candidates' y (R6) ---- */
     if (model == FMO_ECM) {
-        p->y_s = (double *)malloc(sizeof(double) * (size_t)n);
-        p->ymax = (double *)malloc(sizeof(double) * (size_t)(n + 1));
-        if (!p->y_s || !p->ymax) goto nomem;
-        p->ly_s = (double *)malloc(sizeof(double) * (size_t)n);
-        if (!p->ly_s) goto nomem;
-        for (int64_t r = 0; r < n; r++) p->y_s[r] = y[p->perm[r]];
-        for (int64_t r = 0; r < n; r++) p->ly_s[r] = log(p->y_s[r]);
-        p->ymax[n] = 0.0;
-        for (int64_t t = n - 1; t >= 0; t--) p->ymax[t] = fmax(p->y_s[t], p->ymax[t + 1]);
+        p->ymax = (double *)malloc(sizeof(double) * (size_t)(nc + 1));
+        if (!p->ymax) goto nomem;
+        p->ymax[nc] = 0.0;
+        for (int64_t t = nc - 1; t >= 0; t--) p->ymax[t] = fmax(p->cy[t], p->ymax[t + 1]);
     }
 
     /* ---- a4: planner (not in the paper -- validity from the memoryless skip,
      *      P:L117-124, which lets a row restart with a fresh bound at any candidate) ---- */
     {
         int e = 0;
-        if (p->kappa_s[0] > 0.0) frexp(p->kappa_s[0], &e);
-        p->F = 61 - e - ceil_log2_i64(n);
-        p->P = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(n + 1));
+        if (p->ckappa[0] > 0.0) frexp(p->ckappa[0], &e);
+        p->F = 61 - e - ceil_log2_i64(nc);
+        p->P = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(nc + 1));
         p->row_seg = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
         if (!p->P || !p->row_seg) goto nomem;
         p->P[0] = 0;
-        for (int64_t v = 0; v < n; v++)
-            p->P[v + 1] = p->P[v] + (uint64_t)floor(ldexp(p->kappa_s[v], p->F));
+        for (int64_t v = 0; v < nc; v++)
+            p->P[v + 1] = p->P[v] + (uint64_t)floor(ldexp(p->ckappa[v], p->F));
     }
     /* pass 1: segment counts per row */
     const int64_t unit = (int64_t)1 << FMO_G;
@@ -198,12 +240,13 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
     int64_t nseg = 0;
     for (int64_t i = 0; i < n; i++) {
         p->row_seg[i] = nseg;
-        if (i == n - 1) { m[i] = 0; continue; } /* last row: no candidates, no draws */
+        const int64_t c0 = row_c0(p, i);
+        if (c0 >= nc) { m[i] = 0; continue; } /* no candidates (the last undirected row), no draws */
         double r = p->kappa_s[i];
-        if (model == FMO_ECM) r = p->kappa_s[i] / (1.0 - p->y_s[i] * p->ymax[i + 1]);
-        int64_t s = i + 1; /* smallest v in [i+1, n] with v == n or r*kappa_s[v] < 1 (linear scan) */
-        while (s < n && !(r * p->kappa_s[s] < 1.0)) s++;
-        int64_t Wt = plan_W(p, i, r, s, n) + unit;
+        if (model == FMO_ECM) r = p->kappa_s[i] / (1.0 - p->y_s[i] * p->ymax[c0]);
+        int64_t s = c0; /* smallest v in [c0, nc] with v == nc or r*ckappa[v] < 1 (linear scan) */
+        while (s < nc && !(r * p->ckappa[s] < 1.0)) s++;
+        int64_t Wt = plan_W(p, c0, r, s, nc) + unit;
         int64_t mi = (Wt + seg_target * unit - 1) / (seg_target * unit);
         rr[i] = r; sat[i] = s; wtot[i] = Wt; m[i] = mi;
         nseg += mi;
@@ -225,23 +268,23 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
     }
     /* pass 2: cuts and segments */
     int bad = 0;
-    for (int64_t i = 0; i < n - 1 && !bad; i++) {
-        int64_t g0 = p->row_seg[i], mi = m[i];
-        int64_t prev = i + 1;
+    for (int64_t i = 0; i < n && !bad; i++) {
+        const int64_t g0 = p->row_seg[i], mi = m[i], c0 = row_c0(p, i);
+        int64_t prev = c0;
         for (int64_t k = 0; k < mi; k++) {
             int64_t a = prev, b;
             if (k == mi - 1) {
-                b = n;
+                b = nc;
             } else {
-                /* cut k+1: smallest v in [i+2, n-1] with W_i(v) >= floor((k+1) Wtot / m) */
+                /* cut k+1: smallest v in [c0+1, nc-1] with W(v) >= floor((k+1) Wtot / m) */
                 int64_t theta = (int64_t)(((__int128)(k + 1) * (__int128)wtot[i]) / (__int128)mi);
-                int64_t lo = i + 2, hi = n - 1; /* answer in [lo, hi]; hi if none */
+                int64_t lo = c0 + 1, hi = nc - 1; /* answer in [lo, hi]; hi if none */
                 while (lo < hi) {
                     int64_t mid = lo + (hi - lo) / 2;
-                    if (plan_W(p, i, rr[i], sat[i], mid) >= theta) hi = mid; else lo = mid + 1;
+                    if (plan_W(p, c0, rr[i], sat[i], mid) >= theta) hi = mid; else lo = mid + 1;
                 }
                 b = lo;
-                if (!(b > a) || !(b < n)) { bad = 1; break; } /* cannot happen for S >= 8 */
+                if (!(b > a) || !(b < nc)) { bad = 1; break; } /* cannot happen for S >= 8 */
             }
             int64_t g = g0 + k;
             p->seg_u[g] = (int32_t)i; p->seg_a[g] = (int32_t)a; p->seg_b[g] = (int32_t)b;
@@ -251,14 +294,16 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
     }
     free(m); free(rr); free(sat); free(wtot);
     if (bad) { fmo_plan_free(p); return FMO_ERR_STATE; }
-    /* initial bound of every segment at the virtual previous position a-1 (reading R3), kept as
-     * numerator x0 and denominator d0 of q = x0/d0 (reading R10):
+    /* initial bound of every segment at the virtual previous position a-1 (reading R3; the first
+     * candidate itself when a = 0 in the bipartite case), kept as numerator x0 and denominator d0
+     * of q = x0/d0 (reading R10):
      * UBCM q = X/(1+X), X = kappa_i kappa_{a-1}; -log(1-q) = log1p(X)
      * ECM  q = z/(1-T+z), z = kappa_i kappa_{a-1}, T = y_i ymax[a]; -log(1-q) = log1p(z/(1-T)),
      *      with z/(1-T) evaluated as z * RN(1/(1-T)) */
     for (int64_t g = 0; g < nseg; g++) {
         int64_t i = p->seg_u[g], a = p->seg_a[g];
-        double kq = p->kappa_s[i] * p->kappa_s[a - 1];
+        int64_t bp = a > 0 ? a - 1 : 0;
+        double kq = p->kappa_s[i] * p->ckappa[bp];
         p->seg_x0[g] = kq;
         if (model == FMO_UBCM) {
             p->seg_omT[g] = 1.0;
@@ -278,12 +323,18 @@ int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int6
     *out = p;
     return FMO_OK;
 nomem:
-    free(keys);
     fmo_plan_free(p);
     return FMO_ERR_NOMEM;
 }
 
+int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int64_t seg_target,
+                    fmo_plan **out)
+{
+    return fmo_plan_create2(model, FMO_UNDIRECTED, n, x, y, n, x, y, seg_target, out);
+}
+
 int64_t fmo_plan_n(const fmo_plan *p) { return p->n; }
+int64_t fmo_plan_nc(const fmo_plan *p) { return p->nc; }
 int64_t fmo_plan_nseg(const fmo_plan *p) { return p->nseg; }
 int fmo_plan_F(const fmo_plan *p) { return p->F; }
 
@@ -292,12 +343,12 @@ void fmo_plan_export(const fmo_plan *p, int32_t *perm, double *kappa_s, double *
                      double *seg_h0, double *seg_x0, double *seg_d0, double *seg_omT, double *seg_iomT,
                      double *ly_s)
 {
-    size_t n = (size_t)p->n, s = (size_t)p->nseg;
+    size_t n = (size_t)p->n, nc = (size_t)p->nc, s = (size_t)p->nseg;
     if (perm) memcpy(perm, p->perm, n * sizeof(int32_t));
     if (kappa_s) memcpy(kappa_s, p->kappa_s, n * sizeof(double));
     if (y_s && p->y_s) memcpy(y_s, p->y_s, n * sizeof(double));
-    if (ymax && p->ymax) memcpy(ymax, p->ymax, (n + 1) * sizeof(double));
-    if (P) memcpy(P, p->P, (n + 1) * sizeof(uint64_t));
+    if (ymax && p->ymax) memcpy(ymax, p->ymax, (nc + 1) * sizeof(double));
+    if (P) memcpy(P, p->P, (nc + 1) * sizeof(uint64_t));
     if (seg_u) memcpy(seg_u, p->seg_u, s * sizeof(int32_t));
     if (seg_a) memcpy(seg_a, p->seg_a, s * sizeof(int32_t));
     if (seg_b) memcpy(seg_b, p->seg_b, s * sizeof(int32_t));
@@ -308,6 +359,20 @@ void fmo_plan_export(const fmo_plan *p, int32_t *perm, double *kappa_s, double *
     if (seg_omT) memcpy(seg_omT, p->seg_omT, s * sizeof(double));
     if (seg_iomT) memcpy(seg_iomT, p->seg_iomT, s * sizeof(double));
     if (ly_s && p->ly_s) memcpy(ly_s, p->ly_s, n * sizeof(double));
+}
+
+void fmo_plan_export_cand(const fmo_plan *p, int32_t *cperm, double *ckappa, double *cy, double *cly,
+                          int32_t *excl)
+{
+    size_t nc = (size_t)p->nc, n = (size_t)p->n;
+    if (cperm) memcpy(cperm, p->cperm, nc * sizeof(int32_t));
+    if (ckappa) memcpy(ckappa, p->ckappa, nc * sizeof(double));
+    if (cy && p->cy) memcpy(cy, p->cy, nc * sizeof(double));
+    if (cly && p->cly) memcpy(cly, p->cly, nc * sizeof(double));
+    if (excl) {
+        if (p->excl) memcpy(excl, p->excl, n * sizeof(int32_t));
+        else for (size_t u = 0; u < n; u++) excl[u] = -1;
+    }
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -330,7 +395,9 @@ typedef struct {
     int err;
 } buf_t;
 
-static void buf_push(buf_t *b, int32_t s, int32_t d, int32_t w)
+/* undirected pairs are stored as (min id, max id); bipartite (+ id, - id) and directed (out, in)
+ * pairs as they are (ordered != 0) */
+static void buf_push(buf_t *b, int32_t s, int32_t d, int32_t w, int ordered)
 {
     if (b->err) return;
     if (b->n == b->cap) {
@@ -343,8 +410,8 @@ static void buf_push(buf_t *b, int32_t s, int32_t d, int32_t w)
         b->w = nw;
         b->cap = nc;
     }
-    b->e[2 * b->n] = s < d ? s : d;
-    b->e[2 * b->n + 1] = s < d ? d : s;
+    b->e[2 * b->n] = (ordered || s < d) ? s : d;
+    b->e[2 * b->n + 1] = (ordered || s < d) ? d : s;
     b->w[b->n] = w;
     b->n++;
 }
@@ -389,11 +456,14 @@ static void chain_ubcm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs,
     const int64_t i = p->seg_u[g], b = p->seg_b[g];
     const uint32_t sigma = (uint32_t)p->seg_sigma[g];
     const double kappa_i = p->kappa_s[i];
-    int64_t j = p->seg_a[g] - 1;  /* last evaluated position (virtual a-1 at the start)       */
+    int64_t j = p->seg_a[g] - 1;  /* last evaluated position (virtual a-1 at the start; -1 at a
+                                   * bipartite row start: the bound is then the first candidate) */
     double xq = p->seg_x0[g];     /* proposal q = xq / dq >= p_ij for every remaining j       */
     double dq = p->seg_d0[g];
     double h = p->seg_h0[g];      /* h = -log(1 - q)                                          */
     const int32_t id_i = p->perm[i];
+    const int ordered = p->kind != FMO_UNDIRECTED;
+    const int64_t excl = p->excl ? p->excl[i] : -1; /* directed: no self loop */
     for (uint32_t d = 0;; d++) {
         uint32_t ctr[4] = {d >> 1, sigma, (uint32_t)i, s_abs}, W[4];
         fmo_philox4x32_10(ctr, key, W);
@@ -405,14 +475,15 @@ static void chain_ubcm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs,
         if (!(R < (double)(b - 1 - j))) break; /* end of candidate list (R5) */
         j = j + 1 + (int64_t)floor(R);
         out->landed++;
+        if (j == excl) continue; /* p = 0: never accepted, q unchanged (still a valid bound) */
         /* p_ij = x_i x_j / (1 + x_i x_j)  (P:L92 with x = e^-alpha), as X / D */
-        double X = kappa_i * p->kappa_s[j];
+        double X = kappa_i * p->ckappa[j];
         double D = 1.0 + X;
         if (X * dq > xq * D * (1.0 + 0x1p-50)) out->err = FMO_ERR_STATE; /* contract p <= q */
         /* accept with probability p/q: u < (X/D) / (xq/dq), cross-multiplied (R10) */
         if ((fmo_u01(w_acc) * xq) * D < X * dq) {
             out->accepted++;
-            buf_push(out, id_i, p->perm[j], 1);
+            buf_push(out, id_i, p->cperm[j], 1, ordered);
         }
         /* q <- p_ij; -log(1 - q) = log1p(X) */
         xq = X;
@@ -433,6 +504,8 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
     double dq = p->seg_d0[g];
     double h = p->seg_h0[g];
     const int32_t id_i = p->perm[i];
+    const int ordered = p->kind != FMO_UNDIRECTED;
+    const int64_t excl = p->excl ? p->excl[i] : -1;
     for (uint32_t d = 0;; d++) {
         uint32_t ctr[4] = {d, sigma, (uint32_t)i, s_abs}, W[4];
         fmo_philox4x32_10(ctr, key, W);
@@ -442,15 +515,16 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
         if (!(R < (double)(b - 1 - j))) break;
         j = j + 1 + (int64_t)floor(R);
         out->landed++;
+        if (j == excl) continue;
         /* Eq. 4 in fitness form: p = z / ((1 - t) + z), z = x_i y_i x_j y_j, t = y_i y_j */
-        double z = kappa_i * p->kappa_s[j];
-        double t = y_i * p->y_s[j];
+        double z = kappa_i * p->ckappa[j];
+        double t = y_i * p->cy[j];
         double Dp = (1.0 - t) + z;
         if (z * dq > zq * Dp * (1.0 + 0x1p-50)) out->err = FMO_ERR_STATE;
         if ((fmo_u01(W[1]) * zq) * Dp < z * dq) { /* Alg. 1 line 10, cross-multiplied (R10) */
             /* Eq. 5: w - 1 ~ Geometric on {0,1,..} with ratio t = y_i y_j; inverse transform
              * with log t = log y_i + log y_j (R8) */
-            double G = floor(log(fmo_u01(W[2])) / (ly_i + p->ly_s[j]));
+            double G = floor(log(fmo_u01(W[2])) / (ly_i + p->cly[j]));
             int32_t w;
             if (G <= 2147483646.0) {
                 w = 1 + (int32_t)G;
@@ -459,7 +533,7 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
                 out->flags |= FMO_FLAG_WEIGHT_SATURATED;
             }
             out->accepted++;
-            buf_push(out, id_i, p->perm[j], w);
+            buf_push(out, id_i, p->cperm[j], w, ordered);
         }
         /* Alg. 1 line 12: q <- p_hat_ij(beta_min) = z / (1 - T + z) (Eq. 6 as equality, R7) */
         zq = z;
@@ -622,11 +696,13 @@ static double pair_p(int model, double xi, double xj, double yi, double yj, doub
     return z / (1.0 - t + z);
 }
 
-int fmo_bruteforce(int model, int64_t n, const double *x, const double *y, uint64_t seed,
-                   int64_t n_samples, fmo_result **out)
+int fmo_bruteforce2(int model, int kind, int64_t n1, const double *x1, const double *y1, int64_t n2,
+                    const double *x2, const double *y2, uint64_t seed, int64_t n_samples, fmo_result **out)
 {
     *out = NULL;
-    if (n < 1 || !x || (model == FMO_ECM && !y) || n_samples < 0) return FMO_ERR_INVALID;
+    if (kind == FMO_UNDIRECTED) { n2 = n1; x2 = x1; y2 = y1; }
+    if (n1 < 1 || n2 < 1 || !x1 || !x2 || (model == FMO_ECM && (!y1 || !y2)) || n_samples < 0) return FMO_ERR_INVALID;
+    if (kind == FMO_DIRECTED && n1 != n2) return FMO_ERR_INVALID;
     xo_t rng;
     uint64_t sm = seed;
     for (int k = 0; k < 4; k++) rng.s[k] = splitmix64(&sm);
@@ -635,18 +711,19 @@ int fmo_bruteforce(int model, int64_t n, const double *x, const double *y, uint6
     int64_t *off = (int64_t *)calloc((size_t)n_samples + 1, sizeof(int64_t));
     if (!off) return FMO_ERR_NOMEM;
     for (int64_t s = 0; s < n_samples; s++) {
-        for (int64_t i = 0; i < n; i++) {
-            for (int64_t j = i + 1; j < n; j++) {
+        for (int64_t i = 0; i < n1; i++) {
+            for (int64_t j = (kind == FMO_UNDIRECTED ? i + 1 : 0); j < n2; j++) {
+                if (kind == FMO_DIRECTED && j == i) continue; /* no self loops */
                 double t;
-                double pij = pair_p(model, x[i], x[j], model == FMO_ECM ? y[i] : 0.0,
-                                    model == FMO_ECM ? y[j] : 0.0, &t);
+                double pij = pair_p(model, x1[i], x2[j], model == FMO_ECM ? y1[i] : 0.0,
+                                    model == FMO_ECM ? y2[j] : 0.0, &t);
                 B.draws++;
                 if (xo_unif(&rng) < pij) {
                     int32_t w = 1;
                     if (model == FMO_ECM)
                         while (xo_unif(&rng) < t && w < INT32_MAX) w++; /* P(w) = t^{w-1}(1-t) */
                     B.accepted++;
-                    buf_push(&B, (int32_t)i, (int32_t)j, w);
+                    buf_push(&B, (int32_t)i, (int32_t)j, w, kind != FMO_UNDIRECTED);
                 }
             }
         }
@@ -666,6 +743,32 @@ int fmo_bruteforce(int model, int64_t n, const double *x, const double *y, uint6
     free(off); free(B.e); free(B.w);
     *out = R;
     return rc;
+}
+
+int fmo_bruteforce(int model, int64_t n, const double *x, const double *y, uint64_t seed,
+                   int64_t n_samples, fmo_result **out)
+{
+    return fmo_bruteforce2(model, FMO_UNDIRECTED, n, x, y, n, x, y, seed, n_samples, out);
+}
+
+/* Closed forms for bipartite / directed ensembles (plain O(N1 N2) sums): for + node i
+ * kout[i] = sum_j p_ij, kout_var[i] = sum_j p_ij (1 - p_ij); for - node j kin[j], kin_var[j]
+ * (directed: j != i).  ECM: p from Eq. 4 with the cross-set fitness. */
+void fmo_expected2(int model, int kind, int64_t n1, const double *x1, const double *y1, int64_t n2,
+                   const double *x2, const double *y2, double *kout, double *kout_var, double *kin,
+                   double *kin_var)
+{
+    for (int64_t i = 0; i < n1; i++) { kout[i] = 0.0; kout_var[i] = 0.0; }
+    for (int64_t j = 0; j < n2; j++) { kin[j] = 0.0; kin_var[j] = 0.0; }
+    for (int64_t i = 0; i < n1; i++) {
+        for (int64_t j = 0; j < n2; j++) {
+            if (kind == FMO_DIRECTED && i == j) continue;
+            double t;
+            double pij = pair_p(model, x1[i], x2[j], model == FMO_ECM ? y1[i] : 0.0, model == FMO_ECM ? y2[j] : 0.0, &t);
+            kout[i] += pij; kout_var[i] += pij * (1.0 - pij);
+            kin[j] += pij; kin_var[j] += pij * (1.0 - pij);
+        }
+    }
 }
 
 /* ------------------------------------------------------------------------------------------ */

@@ -23,6 +23,7 @@ extern "C" {
 #endif
 
 enum { FMO_UBCM = 0, FMO_ECM = 1 };
+enum { FMO_UNDIRECTED = 0, FMO_BIPARTITE = 1, FMO_DIRECTED = 2 }; /* P:L193-201 */
 enum { FMO_OK = 0, FMO_ERR_INVALID = -1, FMO_ERR_NOMEM = -2, FMO_ERR_STATE = -5 };
 enum { FMO_FLAG_WEIGHT_SATURATED = 1u };
 
@@ -36,10 +37,17 @@ double fmo_u01(uint32_t k);
 /* floor(-log(u01(k)) / h) as int64, or -1 when the quotient is >= 2^62 or not finite (skip law). */
 int64_t fmo_skip(uint32_t k, double h);
 
-/* a1-a4: validate, key, sort, suffix max, plan. */
+/* a1-a4: validate, key, sort, suffix max, plan; undirected. */
 int fmo_plan_create(int model, int64_t n, const double *x, const double *y, int64_t seg_target,
                     fmo_plan **out);
+/* bipartite (+ set rows x1,y1 against - set candidates x2,y2) and directed (out-fitness x1,y1,
+ * in-fitness x2,y2, n1 == n2, no self loops) plans; kind FMO_UNDIRECTED ignores set 2 */
+int fmo_plan_create2(int model, int kind, int64_t n1, const double *x1, const double *y1, int64_t n2,
+                     const double *x2, const double *y2, int64_t seg_target, fmo_plan **out);
 void fmo_plan_free(fmo_plan *p);
+int64_t fmo_plan_nc(const fmo_plan *p);
+void fmo_plan_export_cand(const fmo_plan *p, int32_t *cperm, double *ckappa, double *cy, double *cly,
+                          int32_t *excl);
 int64_t fmo_plan_n(const fmo_plan *p);
 int64_t fmo_plan_nseg(const fmo_plan *p);
 int fmo_plan_F(const fmo_plan *p);
@@ -59,6 +67,11 @@ int fmo_sample(const fmo_plan *p, uint64_t seed, int64_t first_sample, int64_t n
  * an unrelated RNG (xoshiro256**), weights by sequential Bernoulli trials (Eq. 3-5). */
 int fmo_bruteforce(int model, int64_t n, const double *x, const double *y, uint64_t seed,
                    int64_t n_samples, fmo_result **out);
+int fmo_bruteforce2(int model, int kind, int64_t n1, const double *x1, const double *y1, int64_t n2,
+                    const double *x2, const double *y2, uint64_t seed, int64_t n_samples, fmo_result **out);
+void fmo_expected2(int model, int kind, int64_t n1, const double *x1, const double *y1, int64_t n2,
+                   const double *x2, const double *y2, double *kout, double *kout_var, double *kin,
+                   double *kin_var);
 
 int64_t fmo_result_n_samples(const fmo_result *r);
 int64_t fmo_result_n_edges(const fmo_result *r);

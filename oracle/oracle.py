@@ -23,6 +23,8 @@ _LIB = os.path.join(_HERE, "libfmo.so")
 
 UBCM, ECM = 0, 1
 _MODELS = {"ubcm": UBCM, "ecm": ECM, UBCM: UBCM, ECM: ECM}
+UNDIRECTED, BIPARTITE, DIRECTED = 0, 1, 2
+_KINDS = {"undirected": UNDIRECTED, "bipartite": BIPARTITE, "directed": DIRECTED, 0: 0, 1: 1, 2: 2}
 
 CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread"]
 
@@ -57,6 +59,19 @@ def lib():
     L.fmo_skip.restype = C.c_int64
     L.fmo_plan_create.argtypes = [C.c_int, C.c_int64, f64p, f64p, C.c_int64, C.POINTER(vp)]
     L.fmo_plan_create.restype = C.c_int
+    L.fmo_plan_create2.argtypes = [C.c_int, C.c_int, C.c_int64, f64p, f64p, C.c_int64, f64p, f64p, C.c_int64,
+                                   C.POINTER(vp)]
+    L.fmo_plan_create2.restype = C.c_int
+    L.fmo_plan_nc.argtypes = [vp]
+    L.fmo_plan_nc.restype = C.c_int64
+    L.fmo_plan_export_cand.argtypes = [vp, i32p, f64p, f64p, f64p, i32p]
+    L.fmo_plan_export_cand.restype = None
+    L.fmo_bruteforce2.argtypes = [C.c_int, C.c_int, C.c_int64, f64p, f64p, C.c_int64, f64p, f64p, C.c_uint64,
+                                  C.c_int64, C.POINTER(vp)]
+    L.fmo_bruteforce2.restype = C.c_int
+    L.fmo_expected2.argtypes = [C.c_int, C.c_int, C.c_int64, f64p, f64p, C.c_int64, f64p, f64p, f64p, f64p, f64p,
+                                f64p]
+    L.fmo_expected2.restype = None
     L.fmo_plan_free.argtypes = [vp]
     L.fmo_plan_free.restype = None
     L.fmo_plan_n.argtypes = [vp]
@@ -142,6 +157,13 @@ class Plan:
     seg_omT: np.ndarray
     seg_iomT: np.ndarray
     ly_s: np.ndarray | None
+    kind: int = UNDIRECTED
+    nc: int = 0
+    cperm: np.ndarray | None = None     # candidate (- set) arrays; the row arrays when undirected
+    ckappa: np.ndarray | None = None
+    cy: np.ndarray | None = None
+    cly: np.ndarray | None = None
+    excl: np.ndarray | None = None      # directed: candidate rank of each row's own node
     _h: int = 0
 
     @property
@@ -157,25 +179,34 @@ class Plan:
             self._h = 0
 
 
-def sort_plan(x, y=None, seg_target: int = 256, model=None) -> Plan:
-    """a1-a4 of the contract."""
+def sort_plan(x, y=None, seg_target: int = 256, model=None, kind=UNDIRECTED, x2=None, y2=None) -> Plan:
+    """a1-a4 of the contract.  kind BIPARTITE: rows (x, y) = the + set,
+    candidates (x2, y2) = the - set; DIRECTED: (x, y) out-fitness, (x2, y2) in-fitness."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     if model is None:
         model = UBCM if y is None else ECM
     model = _MODELS[model]
+    kind = _KINDS[kind]
     yy = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+    if kind == UNDIRECTED:
+        x2a, y2a = x, yy
+    else:
+        x2a = np.ascontiguousarray(x2, dtype=np.float64)
+        y2a = None if y2 is None else np.ascontiguousarray(y2, dtype=np.float64)
     h = C.c_void_p()
-    rc = lib().fmo_plan_create(model, len(x), _p(x, C.c_double), _p(yy, C.c_double), int(seg_target), C.byref(h))
+    rc = lib().fmo_plan_create2(model, kind, len(x), _p(x, C.c_double), _p(yy, C.c_double), len(x2a),
+                                _p(x2a, C.c_double), _p(y2a, C.c_double), int(seg_target), C.byref(h))
     if rc != 0:
         raise OracleError(f"fmo_plan_create failed: {rc}")
     L = lib()
     n = L.fmo_plan_n(h)
+    nc = L.fmo_plan_nc(h)
     ns = L.fmo_plan_nseg(h)
     perm = np.empty(n, np.int32)
     ks = np.empty(n, np.float64)
     ys = np.empty(n, np.float64) if model == ECM else None
-    ym = np.empty(n + 1, np.float64) if model == ECM else None
-    P = np.empty(n + 1, np.uint64)
+    ym = np.empty(nc + 1, np.float64) if model == ECM else None
+    P = np.empty(nc + 1, np.uint64)
     ly = np.empty(n, np.float64) if model == ECM else None
     su, sa, sb, ss = (np.empty(ns, np.int32) for _ in range(4))
     h0, x0, d0, om, iom = (np.empty(ns, np.float64) for _ in range(5))
@@ -183,8 +214,15 @@ def sort_plan(x, y=None, seg_target: int = 256, model=None) -> Plan:
                       _p(P, C.c_uint64), _p(su, C.c_int32), _p(sa, C.c_int32), _p(sb, C.c_int32),
                       _p(ss, C.c_int32), _p(h0, C.c_double), _p(x0, C.c_double), _p(d0, C.c_double),
                       _p(om, C.c_double), _p(iom, C.c_double), _p(ly, C.c_double))
+    cperm = np.empty(nc, np.int32)
+    ck = np.empty(nc, np.float64)
+    cy = np.empty(nc, np.float64) if model == ECM else None
+    cly = np.empty(nc, np.float64) if model == ECM else None
+    excl = np.empty(n, np.int32)
+    L.fmo_plan_export_cand(h, _p(cperm, C.c_int32), _p(ck, C.c_double), _p(cy, C.c_double), _p(cly, C.c_double),
+                           _p(excl, C.c_int32))
     return Plan(model, n, int(seg_target) or 256, L.fmo_plan_F(h), perm, ks, ys, ym, P, su, sa, sb, ss, h0, x0, d0,
-                om, iom, ly, h.value)
+                om, iom, ly, kind, nc, cperm, ck, cy, cly, excl, h.value)
 
 
 @dataclass
@@ -236,14 +274,18 @@ def sample(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, row
     return res
 
 
-def bruteforce(x, y=None, seed: int = 0, n_samples: int = 1) -> Result:
-    """Level-1 oracle: independent Bernoulli per pair (plain definition, Eq. 3-5)."""
+def bruteforce(x, y=None, seed: int = 0, n_samples: int = 1, kind=UNDIRECTED, x2=None, y2=None) -> Result:
+    """Level-1 oracle: independent Bernoulli per pair (plain definition, Eq. 3-5); bipartite
+    pairs (+ i, - j), directed pairs (i, j != i) when kind says so."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     model = UBCM if y is None else ECM
+    kind = _KINDS[kind]
     yy = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+    x2a = x if kind == UNDIRECTED else np.ascontiguousarray(x2, dtype=np.float64)
+    y2a = yy if kind == UNDIRECTED else (None if y2 is None else np.ascontiguousarray(y2, dtype=np.float64))
     h = C.c_void_p()
-    rc = lib().fmo_bruteforce(model, len(x), _p(x, C.c_double), _p(yy, C.c_double), int(seed), int(n_samples),
-                              C.byref(h))
+    rc = lib().fmo_bruteforce2(model, kind, len(x), _p(x, C.c_double), _p(yy, C.c_double), len(x2a),
+                               _p(x2a, C.c_double), _p(y2a, C.c_double), int(seed), int(n_samples), C.byref(h))
     if rc != 0:
         raise OracleError(f"fmo_bruteforce failed: {rc}")
     res = _collect(h)
@@ -266,6 +308,22 @@ def expected(x, y=None, nodes=None, nthreads: int | None = None):
                        int(nthreads or ncores()), _p(k, C.c_double), _p(kv, C.c_double), _p(s, C.c_double),
                        _p(sv, C.c_double))
     return k, kv, s, sv
+
+
+def expected2(x, y, x2, y2, kind=BIPARTITE):
+    """Closed forms of a bipartite/directed ensemble: (kout, kout_var) per + node and (kin, kin_var)
+    per - node."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    x2 = np.ascontiguousarray(x2, dtype=np.float64)
+    model = UBCM if y is None else ECM
+    yy = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+    yy2 = None if y2 is None else np.ascontiguousarray(y2, dtype=np.float64)
+    ko, kov = np.empty(len(x)), np.empty(len(x))
+    ki, kiv = np.empty(len(x2)), np.empty(len(x2))
+    lib().fmo_expected2(model, _KINDS[kind], len(x), _p(x, C.c_double), _p(yy, C.c_double), len(x2),
+                        _p(x2, C.c_double), _p(yy2, C.c_double), _p(ko, C.c_double), _p(kov, C.c_double),
+                        _p(ki, C.c_double), _p(kiv, C.c_double))
+    return ko, kov, ki, kiv
 
 
 def expected_edges(x, y=None, nthreads: int | None = None) -> float:
