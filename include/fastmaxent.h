@@ -46,6 +46,11 @@ typedef enum {
 
 typedef enum { FM_UBCM = 0, FM_ECM = 1 } fm_model;
 
+/* Graph kind (R16).  Undirected: pairs {i, j} of one node set.  Bipartite:
+ * pairs (+i, -j) of two node sets.  Directed: ordered pairs (i, j), i != j, with out-fitness and
+ * in-fitness (the bipartite graph of out- and in-copies without the diagonal). */
+typedef enum { FM_UNDIRECTED = 0, FM_BIPARTITE = 1, FM_DIRECTED = 2 } fm_graph;
+
 enum {
     FM_FLAG_WEIGHT_SATURATED = 1u, /* an ECM weight exceeded INT32_MAX and was clamped (R8) */
     FM_FLAG_SCRATCH_RERUN = 2u     /* some chunks overflowed their scratch and were re-run (same result) */
@@ -61,8 +66,9 @@ typedef struct {
     int64_t n_samples;
     int64_t n_edges;   /* total over all samples */
     int64_t *offsets;  /* HOST int64[n_samples + 1]: sample s = edges[offsets[s] .. offsets[s+1]) */
-    int32_t *edges;    /* DEVICE int32[2 * n_edges]: pairs (src, dst), src < dst, original ids
-                          ("Edge list E"; no self loops, no duplicates)                    */
+    int32_t *edges;    /* DEVICE int32[2 * n_edges]: pairs in original ids ("Edge list E"; no
+                          duplicates): undirected (src, dst) with src < dst, no self loops;
+                          bipartite (+ id, - id); directed (source, target), no self loops      */
     int32_t *weights;  /* DEVICE int32[n_edges] (ECM, w >= 1), NULL for UBCM                         */
     int64_t draws;     /* counters summed over samples: geometric draws incl. terminal ones     */
     int64_t landed;    /* proposals (candidates reached, p/q tests)                              */
@@ -75,6 +81,8 @@ typedef struct {
 
 typedef struct {
     int32_t model;
+    int32_t kind;         /* fm_graph */
+    int64_t n_minus;      /* candidates: the - set (bipartite), in-copies (directed), == n undirected */
     int64_t n;
     int64_t seg_target;
     int32_t F;            /* fixed-point exponent of the planner (DESIGN.md 3.4 step 1) */
@@ -90,6 +98,15 @@ typedef struct {
  * otherwise 8 <= S <= 2^40 (S changes results; R15).  Synchronises the stream once. */
 fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double *y,
                        int64_t seg_target, void *cuda_stream, fm_plan **plan_out);
+
+/* As fm_sort_plan for bipartite (kind FM_BIPARTITE: rows = the + set (x_plus, y_plus), candidates
+ * = the - set (x_minus, y_minus), each sorted by its own key) and directed graphs
+ * (FM_DIRECTED: x_plus/y_plus = out-fitness, x_minus/y_minus = in-fitness, n_plus == n_minus,
+ * self loops excluded).  n_plus, n_minus >= 1.  Sampled with fm_sample_ubcm/ecm. */
+fm_status fm_sort_plan_bipartite(fm_model model, fm_graph kind, int64_t n_plus, const double *x_plus,
+                                 const double *y_plus, int64_t n_minus, const double *x_minus,
+                                 const double *y_minus, int64_t seg_target, void *cuda_stream,
+                                 fm_plan **plan_out);
 
 /* a5-a6.  Draw n_samples graphs (sample indices first_sample .. first_sample+n_samples-1,
  * first_sample + n_samples <= 2^32) from the UBCM with Philox key `seed`.
@@ -119,6 +136,12 @@ fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info);
 fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, double *y_s, double *ymax, double *ly_s,
                          int32_t *seg, double *seg_h0, double *seg_x0, double *seg_d0, double *seg_omT,
                          double *seg_iomT);
+
+/* Inspection of the candidate set of a bipartite/directed plan (the row arrays when undirected):
+ * cperm int32[n_minus], ckappa/cy/cly float64[n_minus], excl int32[n] (directed: candidate rank of
+ * each row's own node, else -1).  Any pointer may be NULL.  Synchronises the current device. */
+fm_status fm_plan_export_candidates(const fm_plan *plan, int32_t *cperm, double *ckappa, double *cy,
+                                    double *cly, int32_t *excl);
 
 /* Device-side phase timing (for benchmarks).  When enabled, CUDA events are recorded on the
  * call's stream around each phase; fm_timing_get synchronises those events and returns the

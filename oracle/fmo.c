@@ -153,6 +153,7 @@ static int sort_set(int model, int64_t n, const double *x, const double *y, int3
         keys[i].id = (int32_t)i;
         if (keys[i].kappa > kmax) kmax = keys[i].kappa;
     }
+    if (!isfinite((kmax * kmax) * (kmax * kmax))) { free(keys); return FMO_ERR_INVALID; } /* R10 products */
     qsort(keys, (size_t)n, sizeof(key_t_), cmp_key);
     *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     *kappa_s = (double *)malloc(sizeof(double) * (size_t)n);
@@ -198,8 +199,9 @@ int fmo_plan_create2(int model, int kind, int64_t n1, const double *x1, const do
         rc = sort_set(model, n2, x2, y2, &p->cperm, &p->ckappa, &p->cy, &p->cly, &kmax2);
         if (rc != FMO_OK) { fmo_plan_free(p); return rc; }
     }
-    /* R10's cross products (X * D with X <= kmax1 * kmax2) stay finite */
-    if (!isfinite((kmax1 * kmax2) * (kmax1 * kmax2))) { fmo_plan_free(p); return FMO_ERR_INVALID; }
+    /* R10's cross products (X * D with X <= kmax1 * kmax2) stay finite: implied by each set's
+     * kmax^4 being finite (checked in sort_set) */
+    (void)kmax1; (void)kmax2;
     if (kind == FMO_DIRECTED) { /* the row node's own in-copy is not a candidate */
         int32_t *crank = (int32_t *)malloc(sizeof(int32_t) * (size_t)nc);
         p->excl = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);

@@ -148,6 +148,13 @@ unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) 
 void plan_release(Plan *p)
 {
     if (!p) return;
+    if (p->cperm && p->cperm != p->perm) {
+        cudaFree(p->cperm);
+        cudaFree(p->ckappa);
+        cudaFree(p->cy);
+        cudaFree(p->cly);
+    }
+    cudaFree(p->excl);
     cudaFree(p->perm);
     cudaFree(p->kappa_s);
     cudaFree(p->y_s);
@@ -186,29 +193,16 @@ extern "C" {
 const char *fm_last_error(void) { return g_err.c_str(); }
 int32_t fm_abi_version(void) { return FM_ABI_VERSION; }
 
-fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double *y, int64_t seg_target,
-                       void *cuda_stream, fm_plan **plan_out)
+// a1 + a2 for one node set: validate, key (+ digit histograms), radix sort, rank-order arrays.
+// Validation failures are OR-ed into sc->flags and read at the planner's one synchronisation.
+struct SortedSet {
+    int32_t *perm = nullptr;
+    double *kappa = nullptr, *y = nullptr, *ly = nullptr;
+};
+
+static fm_status sort_node_set(int model, int64_t n, const double *x, const double *y, PlanScalars *sc, Allocs &tmp,
+                               cudaStream_t st, SortedSet &out)
 {
-    if (!plan_out) return fail(FM_ERR_INVALID, "plan_out is NULL");
-    *plan_out = nullptr;
-    if (model != FM_UBCM && model != FM_ECM) return fail(FM_ERR_INVALID, "unknown model %d", (int)model);
-    if (n < 2 || n > INT32_MAX) return fail(FM_ERR_INVALID, "n = %lld outside [2, 2^31-1]", (long long)n);
-    if (!x) return fail(FM_ERR_INVALID, "x is NULL");
-    if (model == FM_ECM && !y) return fail(FM_ERR_INVALID, "ECM needs y");
-    if (model == FM_UBCM && y) return fail(FM_ERR_INVALID, "UBCM takes no y");
-    if (seg_target == 0) seg_target = 256;
-    if (seg_target < 8 || seg_target > (int64_t(1) << 40))
-        return fail(FM_ERR_INVALID, "seg_target %lld outside [8, 2^40]", (long long)seg_target);
-
-    cudaStream_t st = (cudaStream_t)cuda_stream;
-    int dev = 0;
-    CK(cudaGetDevice(&dev), "cudaGetDevice");
-    configure_pool_once(dev);
-    Allocs tmp(st);
-    PhaseTimer timer;
-    timer.begin(kPhasePlan, st);
-
-    // ---- inputs: host or device ----
     const double *xd = x, *yd = y;
     if (!is_device_ptr(x)) {
         double *t;
@@ -222,11 +216,8 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
         CK(cudaMemcpyAsync(t, y, sizeof(double) * n, cudaMemcpyHostToDevice, st), "copy y");
         yd = t;
     }
-
-    // ---- a1: validate + key ----
     uint64_t *ka, *kb;
     int32_t *ia, *ib;
-    PlanScalars *sc;
     unsigned int *hist;
     CK(tmp.get(&hist, 8 * 256), "alloc hist");
     CK(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * 8 * 256, st), "memset hist");
@@ -234,22 +225,78 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     CK(tmp.get(&kb, n), "alloc keys");
     CK(tmp.get(&ia, n), "alloc ids");
     CK(tmp.get(&ib, n), "alloc ids");
+    count_launch();
+    k_validate_key<<<grid_for(n, 256), 256, 0, st>>>(model, n, xd, yd, ka, ia, sc, hist);
+    CK(cudaGetLastError(), "k_validate_key");
+    const size_t tb = radix_tmp_bytes(n);
+    char *work;
+    CK(tmp.get(&work, tb), "alloc sort tmp");
+    uint64_t *skeys;
+    int32_t *perm;
+    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, ~0ull /* all 8 digit passes; a constant digit is a stable copy */, hist,
+                          &skeys, &perm, work, tb, st),
+       "radix sort");
+    tmp.release(perm);
+    out.perm = perm;  // adopted by the plan (freed by plan_release)
+    CK(cudaMallocAsync((void **)&out.kappa, sizeof(double) * n, st), "alloc kappa_s");
+    if (model == FM_ECM) {
+        CK(cudaMallocAsync((void **)&out.y, sizeof(double) * n, st), "alloc y_s");
+        CK(cudaMallocAsync((void **)&out.ly, sizeof(double) * n, st), "alloc ly_s");
+    }
+    count_launch();
+    k_gather_sorted<<<grid_for(n, 256), 256, 0, st>>>(model, n, skeys, yd, out.perm, out.kappa, out.y, out.ly);
+    CK(cudaGetLastError(), "k_gather_sorted");
+    return FM_OK;
+}
+
+static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const double *x1, const double *y1,
+                                int64_t n2, const double *x2, const double *y2, int64_t seg_target,
+                                void *cuda_stream, fm_plan **plan_out)
+{
+    if (!plan_out) return fail(FM_ERR_INVALID, "plan_out is NULL");
+    *plan_out = nullptr;
+    if (model != FM_UBCM && model != FM_ECM) return fail(FM_ERR_INVALID, "unknown model %d", (int)model);
+    if (kind != FM_UNDIRECTED && kind != FM_BIPARTITE && kind != FM_DIRECTED)
+        return fail(FM_ERR_INVALID, "unknown graph kind %d", (int)kind);
+    if (kind == FM_UNDIRECTED) {
+        n2 = n1;
+        x2 = x1;
+        y2 = y1;
+    }
+    const int64_t nmin = kind == FM_UNDIRECTED ? 2 : 1;
+    if (n1 < nmin || n1 > INT32_MAX) return fail(FM_ERR_INVALID, "n = %lld outside [%lld, 2^31-1]", (long long)n1,
+                                                  (long long)nmin);
+    if (n2 < 1 || n2 > INT32_MAX) return fail(FM_ERR_INVALID, "n_minus = %lld outside [1, 2^31-1]", (long long)n2);
+    if (kind == FM_DIRECTED && n1 != n2) return fail(FM_ERR_INVALID, "directed: out and in sets differ in size");
+    if (!x1 || !x2) return fail(FM_ERR_INVALID, "x is NULL");
+    if (model == FM_ECM && (!y1 || !y2)) return fail(FM_ERR_INVALID, "ECM needs y");
+    if (model == FM_UBCM && (y1 || (kind != FM_UNDIRECTED && y2))) return fail(FM_ERR_INVALID, "UBCM takes no y");
+    if (seg_target == 0) seg_target = 256;
+    if (seg_target < 8 || seg_target > (int64_t(1) << 40))
+        return fail(FM_ERR_INVALID, "seg_target %lld outside [8, 2^40]", (long long)seg_target);
+
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    int dev = 0;
+    CK(cudaGetDevice(&dev), "cudaGetDevice");
+    configure_pool_once(dev);
+    Allocs tmp(st);
+    PhaseTimer timer;
+    timer.begin(kPhasePlan, st);
+
+    PlanScalars *sc;
     CK(tmp.get(&sc, 1), "alloc scalars");
     PlanScalars h_sc;
     memset(&h_sc, 0, sizeof(h_sc));
     h_sc.key_and = ~0ull;
     CK(cudaMemcpyAsync(sc, &h_sc, sizeof(h_sc), cudaMemcpyHostToDevice, st), "init scalars");
-    count_launch();
-    k_validate_key<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, xd, yd, ka, ia, sc, hist);
-    CK(cudaGetLastError(), "k_validate_key");
-    // (no sync here: the validation flag is read with the segment count below; the kernels in
-    //  between are harmless on invalid input)
 
     Plan *p = new Plan();
     memset(p, 0, sizeof(Plan));
     p->magic = kPlanMagic;
     p->model = (int)model;
-    p->n = n;
+    p->kind = (int)kind;
+    p->n = n1;
+    p->nc = n2;
     p->S = seg_target;
     p->device = dev;
     struct PlanGuard {
@@ -257,51 +304,70 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
         ~PlanGuard() { if (p) plan_release(p); }
     } guard{p};
 
-    // ---- a2: sort ----
-    size_t tmp_bytes = std::max(radix_tmp_bytes(n), scan_tmp_bytes(n + 1) + 256);
-    void *work;
-    CK(tmp.get((char **)&work, tmp_bytes), "alloc sort tmp");
-    uint64_t *skeys;
-    int32_t *perm;
-    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, ~0ull /* all 8 digit passes; a constant digit is a stable copy */,
-                          hist, &skeys, &perm, work,
-                          tmp_bytes, st),
-       "radix sort");
-    tmp.release(perm);
-    p->perm = perm;  // adopt the sorted id buffer (freed by plan_release via cudaFree)
-    CK(cudaMallocAsync((void **)&p->kappa_s, sizeof(double) * n, st), "alloc kappa_s");
-    if (model == FM_ECM) {
-        CK(cudaMallocAsync((void **)&p->y_s, sizeof(double) * n, st), "alloc y_s");
-        CK(cudaMallocAsync((void **)&p->ly_s, sizeof(double) * n, st), "alloc ly_s");
-        CK(cudaMallocAsync((void **)&p->ymax, sizeof(double) * (n + 1), st), "alloc ymax");
+    // ---- a1 + a2: the row set (and the candidate set) ----
+    {
+        SortedSet r;
+        fm_status s = sort_node_set((int)model, n1, x1, y1, sc, tmp, st, r);
+        if (s != FM_OK) return s;
+        p->perm = r.perm;
+        p->kappa_s = r.kappa;
+        p->y_s = r.y;
+        p->ly_s = r.ly;
     }
-    count_launch();
-    k_gather_sorted<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, skeys, yd, p->perm, p->kappa_s, p->y_s,
-                                                      p->ly_s);
-    CK(cudaGetLastError(), "k_gather_sorted");
+    if (kind == FM_UNDIRECTED) {
+        p->cperm = p->perm;
+        p->ckappa = p->kappa_s;
+        p->cy = p->y_s;
+        p->cly = p->ly_s;
+    } else {
+        SortedSet c;
+        fm_status s = sort_node_set((int)model, n2, x2, y2, sc, tmp, st, c);
+        if (s != FM_OK) return s;
+        p->cperm = c.perm;
+        p->ckappa = c.kappa;
+        p->cy = c.y;
+        p->cly = c.ly;
+    }
+    const int64_t nc = n2;
+    const size_t sb = scan_tmp_bytes(std::max(n1, nc) + 1) + 256;
+    char *work;
+    CK(tmp.get(&work, sb), "alloc scan tmp");
+    if (kind == FM_DIRECTED) {
+        int32_t *crank;
+        CK(tmp.get(&crank, nc), "alloc crank");
+        CK(cudaMallocAsync((void **)&p->excl, sizeof(int32_t) * n1, st), "alloc excl");
+        count_launch();
+        k_rank_of<<<grid_for(nc, 256), 256, 0, st>>>(nc, p->cperm, crank);
+        count_launch();
+        k_excl<<<grid_for(n1, 256), 256, 0, st>>>(n1, p->perm, crank, p->excl);
+        CK(cudaGetLastError(), "k_excl");
+    }
 
-    // ---- a3: suffix max of y (beta_min) ----
-    if (model == FM_ECM) CK(suffix_max_f64(p->y_s, p->ymax, n, work, tmp_bytes, st), "suffix max");
+    // ---- a3: suffix max of the candidates' y (beta_min) ----
+    if (model == FM_ECM) {
+        CK(cudaMallocAsync((void **)&p->ymax, sizeof(double) * (nc + 1), st), "alloc ymax");
+        CK(suffix_max_f64(p->cy, p->ymax, nc, work, sb, st), "suffix max");
+    }
 
     // ---- a4: planner ----
     uint64_t *P;
     RowInfo *rows;
     int64_t *row_m;
-    CK(tmp.get(&P, n + 1), "alloc P");
-    CK(tmp.get(&rows, n), "alloc rows");
-    CK(tmp.get(&row_m, n + 1), "alloc row_m");
+    CK(tmp.get(&P, nc + 1), "alloc P");
+    CK(tmp.get(&rows, n1), "alloc rows");
+    CK(tmp.get(&row_m, n1 + 1), "alloc row_m");
     count_launch();
-    k_kfx<<<grid_for(n, 256), 256, 0, st>>>(n, ceil_log2(n), p->kappa_s, sc, P);
+    k_kfx<<<grid_for(nc, 256), 256, 0, st>>>(nc, ceil_log2(nc), p->ckappa, sc, P);
     CK(cudaGetLastError(), "k_kfx");
-    CK(scan_exclusive_u64(P, P, n, work, tmp_bytes, st), "scan P");
+    CK(scan_exclusive_u64(P, P, nc, work, sb, st), "scan P");
     count_launch();
-    k_rows<<<grid_for(n, 256), 256, 0, st>>>((int)model, n, seg_target, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
-                                             row_m);
+    k_rows<<<grid_for(n1, 256), 256, 0, st>>>((int)model, (int)kind, n1, nc, seg_target, p->kappa_s, p->y_s,
+                                              p->ckappa, p->ymax, P, sc, rows, row_m);
     CK(cudaGetLastError(), "k_rows");
-    CK(scan_exclusive_i64(row_m, row_m, n, work, tmp_bytes, st), "scan rows");
+    CK(scan_exclusive_i64(row_m, row_m, n1, work, sb, st), "scan rows");
     int64_t n_seg = 0;
     CK(cudaMemcpyAsync(&h_sc, sc, sizeof(h_sc), cudaMemcpyDeviceToHost, st), "read scalars");
-    CK(cudaMemcpyAsync(&n_seg, row_m + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "read n_seg");
+    CK(cudaMemcpyAsync(&n_seg, row_m + n1, sizeof(int64_t), cudaMemcpyDeviceToHost, st), "read n_seg");
     CK(cudaStreamSynchronize(st), "sync (rows)");
     if (h_sc.flags & kErrInvalid)
         return fail(FM_ERR_INVALID, "invalid fitness: x must be finite >= 0, y in [0,1), kappa_max^4 finite");
@@ -319,13 +385,13 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     int64_t *seg_work;
     CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
     count_launch();
-    k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n, n_seg, p->kappa_s, p->y_s, p->ymax, P, sc, rows,
-                                                 row_m, p->sa, seg_work);
+    k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, (int)kind, n1, nc, n_seg, p->kappa_s, p->y_s, p->ckappa,
+                                                 p->ymax, P, sc, rows, row_m, p->sa, seg_work);
     CK(cudaGetLastError(), "k_emit");
     CK(cudaMallocAsync((void **)&p->rec, sizeof(SegRec) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
     count_launch();
     k_pack<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n_seg, p->sa, p->kappa_s, p->perm, p->y_s, p->ly_s,
-                                                 p->rec);
+                                                 p->excl, p->rec);
     CK(cudaGetLastError(), "k_pack");
     {
         const size_t wb = scan_tmp_bytes(n_seg + 1);
@@ -363,7 +429,7 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     }
 
     // the cut invariant (kErrState, impossible for S >= 8) is checked lazily by fm_sample_*: the
-    // plan keeps the flag word on the device and returns without a third synchronisation
+    // plan keeps the flag word on the device and returns without a second synchronisation
     CK(cudaMallocAsync((void **)&p->dev_flags, sizeof(unsigned int), st), "alloc flags");
     CK(cudaMemcpyAsync(p->dev_flags, &sc->flags, sizeof(unsigned int), cudaMemcpyDeviceToDevice, st), "copy flags");
     timer.end(st);
@@ -375,6 +441,24 @@ fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double 
     }
     *plan_out = (fm_plan *)p;
     return FM_OK;
+}
+
+fm_status fm_sort_plan(fm_model model, int64_t n, const double *x, const double *y, int64_t seg_target,
+                       void *cuda_stream, fm_plan **plan_out)
+{
+    return sort_plan_impl(model, FM_UNDIRECTED, n, x, y, n, x, y, seg_target, cuda_stream, plan_out);
+}
+
+fm_status fm_sort_plan_bipartite(fm_model model, fm_graph kind, int64_t n_plus, const double *x_plus,
+                                 const double *y_plus, int64_t n_minus, const double *x_minus, const double *y_minus,
+                                 int64_t seg_target, void *cuda_stream, fm_plan **plan_out)
+{
+    if (kind == FM_UNDIRECTED) {
+        if (plan_out) *plan_out = nullptr;
+        return fail(FM_ERR_INVALID, "fm_sort_plan_bipartite needs FM_BIPARTITE or FM_DIRECTED");
+    }
+    return sort_plan_impl(model, kind, n_plus, x_plus, y_plus, n_minus, x_minus, y_minus, seg_target, cuda_stream,
+                          plan_out);
 }
 
 static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
@@ -447,10 +531,11 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         SampleArgs a;
         memset(&a, 0, sizeof(a));
         a.rec = p->rec;
-        a.kappa_s = p->kappa_s;
-        a.y_s = p->y_s;
-        a.ly_s = p->ly_s;
-        a.perm = p->perm;
+        a.kappa_s = p->ckappa;  // candidates (R16): the - set, or the rows themselves
+        a.y_s = p->cy;
+        a.ly_s = p->cly;
+        a.perm = p->cperm;
+        a.ordered = p->kind != FM_UNDIRECTED;
         a.chunk_seg = p->chunk_seg;
         a.chunk_cap = p->chunk_cap;
         a.n_chunks = p->n_chunks;
@@ -568,6 +653,8 @@ fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info)
     if (!plan || !plan_live(plan)) return fail(FM_ERR_STATE, "not a live fm_plan");
     const Plan *p = (const Plan *)plan;
     info->model = p->model;
+    info->kind = p->kind;
+    info->n_minus = p->nc;
     info->n = p->n;
     info->seg_target = p->S;
     info->F = p->F;
@@ -588,7 +675,7 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (perm) CK(cudaMemcpy(perm, p->perm, n * 4, cudaMemcpyDeviceToHost), "perm");
     if (kappa_s) CK(cudaMemcpy(kappa_s, p->kappa_s, n * 8, cudaMemcpyDeviceToHost), "kappa_s");
     if (y_s && p->y_s) CK(cudaMemcpy(y_s, p->y_s, n * 8, cudaMemcpyDeviceToHost), "y_s");
-    if (ymax && p->ymax) CK(cudaMemcpy(ymax, p->ymax, (n + 1) * 8, cudaMemcpyDeviceToHost), "ymax");
+    if (ymax && p->ymax) CK(cudaMemcpy(ymax, p->ymax, ((size_t)p->nc + 1) * 8, cudaMemcpyDeviceToHost), "ymax");
     if (ly_s && p->ly_s) CK(cudaMemcpy(ly_s, p->ly_s, n * 8, cudaMemcpyDeviceToHost), "ly_s");
     if (seg && s) CK(cudaMemcpy(seg, p->sa.seg, s * 16, cudaMemcpyDeviceToHost), "seg");
     if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->sa.h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
@@ -596,6 +683,24 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (seg_d0 && s) CK(cudaMemcpy(seg_d0, p->sa.d0, s * 8, cudaMemcpyDeviceToHost), "seg_d0");
     if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->sa.omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
     if (seg_iomT && s) CK(cudaMemcpy(seg_iomT, p->sa.iomT, s * 8, cudaMemcpyDeviceToHost), "seg_iomT");
+    return FM_OK;
+}
+
+fm_status fm_plan_export_candidates(const fm_plan *plan, int32_t *cperm, double *ckappa, double *cy, double *cly,
+                                    int32_t *excl)
+{
+    if (!plan || !plan_live(plan)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan;
+    CK(cudaDeviceSynchronize(), "sync");
+    const size_t nc = (size_t)p->nc, n = (size_t)p->n;
+    if (cperm) CK(cudaMemcpy(cperm, p->cperm, nc * 4, cudaMemcpyDeviceToHost), "cperm");
+    if (ckappa) CK(cudaMemcpy(ckappa, p->ckappa, nc * 8, cudaMemcpyDeviceToHost), "ckappa");
+    if (cy && p->cy) CK(cudaMemcpy(cy, p->cy, nc * 8, cudaMemcpyDeviceToHost), "cy");
+    if (cly && p->cly) CK(cudaMemcpy(cly, p->cly, nc * 8, cudaMemcpyDeviceToHost), "cly");
+    if (excl) {
+        if (p->excl) CK(cudaMemcpy(excl, p->excl, n * 4, cudaMemcpyDeviceToHost), "excl");
+        else for (size_t u = 0; u < n; u++) excl[u] = -1;
+    }
     return FM_OK;
 }
 

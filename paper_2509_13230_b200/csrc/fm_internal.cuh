@@ -26,7 +26,7 @@ struct __align__(16) SegRec {
     int32_t u, a, b, sigma;  // focal rank, candidates [a, b), segment index in the row
     double h0, x0;           // initial bound at a-1: q0 = x0 / d0, h0 = -log(1 - q0)
     double d0, ku;           // ..., kappa_s[u]
-    int32_t id_u, pad0, pad1, pad2;  // perm[u]
+    int32_t id_u, excl, pad1, pad2;  // perm[u]; directed: candidate rank of u's own node, else -1
     double yu, ly_u;         // ECM: y_s[u], log y_s[u]
     double omT, iomT;        // ECM: 1 - T, RN(1 / (1 - T))
 };
@@ -40,14 +40,19 @@ struct SegArrays {
 struct Plan {
     uint32_t magic;
     int model;
-    int64_t n, S;
+    int kind;           // FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED (R16)
+    int64_t n, nc, S;   // rows (+ set), candidates (- set; == n undirected)
     int F;
     int device;
     // a2/a3 (rank space)
     int32_t *perm;      // [n] rank -> id
     double *kappa_s;    // [n]
     double *y_s;        // [n] ECM
-    double *ymax;       // [n+1] ECM
+    double *ymax;       // [nc+1] ECM, over the candidates
+    // candidates (the - set); aliases of the row arrays when undirected
+    int32_t *cperm;
+    double *ckappa, *cy, *cly;
+    int32_t *excl;      // [n] directed: candidate rank of each row's own node
     // a4 segments
     int64_t n_seg;
     SegArrays sa;       // [n_seg] each

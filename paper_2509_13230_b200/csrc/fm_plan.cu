@@ -100,41 +100,48 @@ __global__ void __launch_bounds__(256) k_kfx(int64_t n, int L, const double *__r
     kfx[v] = (uint64_t)floor(ldexp(kappa_s[v], F));
 }
 
-// a4 step 3-4 (per row): r_u, sat_u, Wtot_u, m_u
-__global__ void __launch_bounds__(256) k_rows(int model, int64_t n, int64_t S, const double *__restrict__ kappa_s,
-                                              const double *__restrict__ y_s, const double *__restrict__ ymax,
+// first candidate of row u: undirected j > u; bipartite / directed every - node
+__device__ __forceinline__ int64_t row_c0(int kind, int64_t u) { return kind == FM_UNDIRECTED ? u + 1 : 0; }
+
+// a4 step 3-4 (per row): r_u, sat_u, Wtot_u, m_u.  Rows: kappa_s/y_s (n); candidates: ckappa/ymax (nc).
+__global__ void __launch_bounds__(256) k_rows(int model, int kind, int64_t n, int64_t nc, int64_t S,
+                                              const double *__restrict__ kappa_s, const double *__restrict__ y_s,
+                                              const double *__restrict__ ckappa, const double *__restrict__ ymax,
                                               const uint64_t *__restrict__ P, PlanScalars *sc, RowInfo *__restrict__ rows,
                                               int64_t *__restrict__ row_m)
 {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     long long work = 0, wseg = 0;
-    if (u < n - 1) {
-        const int F = sc->F;
-        double r = kappa_s[u];
-        if (model == FM_ECM) r = __ddiv_rn(kappa_s[u], __dsub_rn(1.0, __dmul_rn(y_s[u], ymax[u + 1])));
-        int64_t sat;
-        if (__dmul_rn(r, kappa_s[u + 1]) < 1.0) {
-            sat = u + 1;
-        } else {  // smallest v in [u+1, n] with v == n or r*kappa_s[v] < 1 (monotone predicate)
-            int64_t lo = u + 2, hi = n;
-            while (lo < hi) {
-                const int64_t mid = lo + ((hi - lo) >> 1);
-                if (__dmul_rn(r, kappa_s[mid]) < 1.0) hi = mid; else lo = mid + 1;
+    if (u < n) {
+        const int64_t c0 = row_c0(kind, u);
+        if (c0 < nc) {
+            const int F = sc->F;
+            double r = kappa_s[u];
+            if (model == FM_ECM) r = __ddiv_rn(kappa_s[u], __dsub_rn(1.0, __dmul_rn(y_s[u], ymax[c0])));
+            int64_t sat;
+            if (__dmul_rn(r, ckappa[c0]) < 1.0) {
+                sat = c0;
+            } else {  // smallest v in [c0, nc] with v == nc or r*ckappa[v] < 1 (monotone predicate)
+                int64_t lo = c0 + 1, hi = nc;
+                while (lo < hi) {
+                    const int64_t mid = lo + ((hi - lo) >> 1);
+                    if (__dmul_rn(r, ckappa[mid]) < 1.0) hi = mid; else lo = mid + 1;
+                }
+                sat = lo;
             }
-            sat = lo;
+            const int64_t WN = plan_W(P, F, c0, r, sat, nc);
+            const int64_t Wt = WN + kUnit;
+            const int64_t m = (Wt + S * kUnit - 1) / (S * kUnit);
+            rows[u].r = r;
+            rows[u].sat = sat;
+            rows[u].wtot = Wt;
+            row_m[u] = m;
+            work = WN + m * kUnit;
+            // bound of one segment's work: Wtot (unsplit) or ceil(Wtot/m) + 2 units + 2 (DESIGN 7.2)
+            wseg = m == 1 ? Wt : (Wt + m - 1) / m + 2 * kUnit + 2;
+        } else {
+            row_m[u] = 0;  // no candidates (the last undirected row): no segment, no draw
         }
-        const int64_t WN = plan_W(P, F, u, r, sat, n);
-        const int64_t Wt = WN + kUnit;
-        const int64_t m = (Wt + S * kUnit - 1) / (S * kUnit);
-        rows[u].r = r;
-        rows[u].sat = sat;
-        rows[u].wtot = Wt;
-        row_m[u] = m;
-        work = WN + m * kUnit;
-        // bound of one segment's work: Wtot (unsplit) or ceil(Wtot/m) + 2 units + 2 (DESIGN 7.2)
-        wseg = m == 1 ? Wt : (Wt + m - 1) / m + 2 * kUnit + 2;
-    } else if (u == n - 1) {
-        row_m[u] = 0;
     }
     // block reduce of work (int64)
 #pragma unroll
@@ -148,23 +155,24 @@ __global__ void __launch_bounds__(256) k_rows(int model, int64_t n, int64_t S, c
     }
 }
 
-// cut k of row u (1 <= k < m): smallest v in [u+2, n-1] with W_u(v) >= floor(k Wtot / m), n-1 if none
-__device__ __forceinline__ int64_t plan_cut(const uint64_t *P, int F, int64_t n, int64_t u, const RowInfo &ri,
+// cut k of row u (1 <= k < m): smallest v in [c0+1, nc-1] with W_u(v) >= floor(k Wtot / m), nc-1 if none
+__device__ __forceinline__ int64_t plan_cut(const uint64_t *P, int F, int64_t nc, int64_t c0, const RowInfo &ri,
                                             int64_t m, int64_t k)
 {
     const int64_t q = ri.wtot / m, rm = ri.wtot - q * m;
     const int64_t theta = k * q + (k * rm) / m;  // == floor(k * Wtot / m) exactly
-    int64_t lo = u + 2, hi = n - 1;
+    int64_t lo = c0 + 1, hi = nc - 1;
     while (lo < hi) {
         const int64_t mid = lo + ((hi - lo) >> 1);
-        if (plan_W(P, F, u, ri.r, ri.sat, mid) >= theta) hi = mid; else lo = mid + 1;
+        if (plan_W(P, F, c0, ri.r, ri.sat, mid) >= theta) hi = mid; else lo = mid + 1;
     }
     return lo;
 }
 
-// a4 step 5-6 (per segment): (u, a, b, sigma), initial bound (q0, h0, omT), work estimate
-__global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_seg, const double *__restrict__ kappa_s,
-                                              const double *__restrict__ y_s, const double *__restrict__ ymax,
+// a4 step 5-6 (per segment): (u, a, b, sigma), initial bound (x0, d0, h0, omT), work estimate
+__global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg,
+                                              const double *__restrict__ kappa_s, const double *__restrict__ y_s,
+                                              const double *__restrict__ ckappa, const double *__restrict__ ymax,
                                               const uint64_t *__restrict__ P, PlanScalars *sc,
                                               const RowInfo *__restrict__ rows, const int64_t *__restrict__ row_seg,
                                               SegArrays sa, int64_t *__restrict__ seg_work)
@@ -172,23 +180,28 @@ __global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_se
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_seg) return;
     const int F = sc->F;
-    // row u: largest u with row_seg[u] <= g; u in [g - extra, g] since every row u < n-1 has >= 1 segment
-    const int64_t extra = n_seg - (n - 1);
-    int64_t lo = g - extra > 0 ? g - extra : 0, hi = g < n - 2 ? g : n - 2;
+    // row u: largest u with row_seg[u] <= g; every row that has candidates has >= 1 segment, so
+    // u lies in [g - extra, g] (rows with candidates: n-1 undirected, all n otherwise)
+    const int64_t rows_w = kind == FM_UNDIRECTED ? n - 1 : n;
+    const int64_t extra = n_seg - rows_w;
+    int64_t lo = g - extra > 0 ? g - extra : 0, hi = g < rows_w - 1 ? g : rows_w - 1;
     while (lo < hi) {
         const int64_t mid = lo + ((hi - lo + 1) >> 1);
         if (row_seg[mid] <= g) lo = mid; else hi = mid - 1;
     }
     const int64_t u = lo;
+    const int64_t c0 = row_c0(kind, u);
     const int64_t sigma = g - row_seg[u];
     const int64_t m = row_seg[u + 1] - row_seg[u];
     const RowInfo ri = rows[u];
     int64_t a, b;
-    a = sigma == 0 ? u + 1 : plan_cut(P, F, n, u, ri, m, sigma);
-    b = sigma == m - 1 ? n : plan_cut(P, F, n, u, ri, m, sigma + 1);
-    if (!(a < b) || !(a > u)) atomicOr(&sc->flags, kErrState);
+    a = sigma == 0 ? c0 : plan_cut(P, F, nc, c0, ri, m, sigma);
+    b = sigma == m - 1 ? nc : plan_cut(P, F, nc, c0, ri, m, sigma + 1);
+    if (!(a < b) || !(a >= c0)) atomicOr(&sc->flags, kErrState);
     sa.seg[g] = make_int4((int)u, (int)a, (int)b, (int)sigma);
-    const double kq = __dmul_rn(kappa_s[u], kappa_s[a - 1]);
+    // bound at the virtual previous position a-1 (R3); a bipartite row start uses candidate 0 (R16)
+    const int64_t bp = a > 0 ? a - 1 : 0;
+    const double kq = __dmul_rn(kappa_s[u], ckappa[bp]);
     sa.x0[g] = kq;
     if (model == FM_UBCM) {
         sa.omT[g] = 1.0;
@@ -204,9 +217,22 @@ __global__ void __launch_bounds__(256) k_emit(int model, int64_t n, int64_t n_se
         sa.d0[g] = __dadd_rn(omT, kq);
         sa.h0[g] = log1p(__dmul_rn(kq, iomT));
     }
-    const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, u, ri.r, ri.sat, a);
-    const int64_t wb = plan_W(P, F, u, ri.r, ri.sat, b);
+    const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, c0, ri.r, ri.sat, a);
+    const int64_t wb = plan_W(P, F, c0, ri.r, ri.sat, b);
     seg_work[g] = wb - wa + kUnit;
+}
+
+// directed (R16): excl[u] = candidate rank of row u's own node (inverse of the candidate order)
+__global__ void k_rank_of(int64_t nc, const int32_t *__restrict__ cperm, int32_t *__restrict__ crank)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < nc) crank[cperm[r]] = (int32_t)r;
+}
+__global__ void k_excl(int64_t n, const int32_t *__restrict__ perm, const int32_t *__restrict__ crank,
+                       int32_t *__restrict__ excl)
+{
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) excl[u] = crank[perm[u]];
 }
 
 // chunking: lane-chunk c starts at the first segment whose work prefix reaches c * target;
@@ -237,7 +263,8 @@ __global__ void __launch_bounds__(256) k_chunks(int64_t n_seg, int64_t n_chunks,
 // packed per-segment records for the sampler (one 64/96-byte read instead of eight gathers)
 __global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, SegArrays sa, const double *__restrict__ kappa_s,
                                               const int32_t *__restrict__ perm, const double *__restrict__ y_s,
-                                              const double *__restrict__ ly_s, SegRec *__restrict__ rec)
+                                              const double *__restrict__ ly_s, const int32_t *__restrict__ excl,
+                                              SegRec *__restrict__ rec)
 {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_seg) return;
@@ -252,7 +279,8 @@ __global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, SegArray
     r.d0 = sa.d0[g];
     r.ku = kappa_s[sg.x];
     r.id_u = perm[sg.x];
-    r.pad0 = r.pad1 = r.pad2 = 0;
+    r.excl = excl ? excl[sg.x] : -1;
+    r.pad1 = r.pad2 = 0;
     r.yu = model == FM_ECM ? y_s[sg.x] : 0.0;
     r.ly_u = model == FM_ECM ? ly_s[sg.x] : 0.0;
     r.omT = sa.omT[g];

@@ -20,11 +20,11 @@ struct RowInfo {
     int64_t wtot;  // Wtot_u
 };
 
-// W_u(v) (DESIGN.md 3.4 step 3): integer estimate of the draws over candidates [u+1, v)
-__device__ __forceinline__ int64_t plan_W(const uint64_t *P, int F, int64_t u, double r, int64_t sat, int64_t v)
+// W_u(v) (DESIGN.md 3.4 step 3): integer estimate of the draws over candidates [c0, v)
+__device__ __forceinline__ int64_t plan_W(const uint64_t *P, int F, int64_t c0, double r, int64_t sat, int64_t v)
 {
     const int64_t vs = v < sat ? v : sat;
-    int64_t W = (vs - u - 1) * kUnit;
+    int64_t W = (vs - c0) * kUnit;
     if (v > sat) {
         const uint64_t D = P[v] - P[sat];
         W += (int64_t)floor(ldexp(__dmul_rn(r, __ull2double_rn(D)), kG - F));
@@ -38,24 +38,27 @@ __global__ void k_gather_sorted(int model, int64_t n, const uint64_t *skeys, con
                                 double *kappa_s, double *y_s, double *ly_s);
 __global__ void k_set_F(int64_t n, int L, const double *kappa_s, PlanScalars *sc);
 __global__ void k_kfx(int64_t n, int L, const double *kappa_s, PlanScalars *sc, uint64_t *kfx);
-__global__ void k_rows(int model, int64_t n, int64_t S, const double *kappa_s, const double *y_s, const double *ymax,
-                       const uint64_t *P, PlanScalars *sc, RowInfo *rows, int64_t *row_m);
-__global__ void k_emit(int model, int64_t n, int64_t n_seg, const double *kappa_s, const double *y_s,
-                       const double *ymax, const uint64_t *P, PlanScalars *sc, const RowInfo *rows,
-                       const int64_t *row_seg, SegArrays sa, int64_t *seg_work);
+__global__ void k_rows(int model, int kind, int64_t n, int64_t nc, int64_t S, const double *kappa_s, const double *y_s,
+                       const double *ckappa, const double *ymax, const uint64_t *P, PlanScalars *sc, RowInfo *rows,
+                       int64_t *row_m);
+__global__ void k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg, const double *kappa_s,
+                       const double *y_s, const double *ckappa, const double *ymax, const uint64_t *P, PlanScalars *sc,
+                       const RowInfo *rows, const int64_t *row_seg, SegArrays sa, int64_t *seg_work);
+__global__ void k_rank_of(int64_t nc, const int32_t *cperm, int32_t *crank);
+__global__ void k_excl(int64_t n, const int32_t *perm, const int32_t *crank, int32_t *excl);
 __global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg,
                          int64_t *chunk_cap);
 __global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap);
 __global__ void k_pack(int model, int64_t n_seg, SegArrays sa, const double *kappa_s, const int32_t *perm,
-                       const double *y_s, const double *ly_s, SegRec *rec);
+                       const double *y_s, const double *ly_s, const int32_t *excl, SegRec *rec);
 
 // ------------------------------------------------------------------------------------------
 // sampler (fm_sample.cu)
 // ------------------------------------------------------------------------------------------
 struct SampleArgs {
     const SegRec *rec;
-    const double *kappa_s, *y_s, *ly_s;
-    const int32_t *perm;
+    const double *kappa_s, *y_s, *ly_s;  // CANDIDATE arrays (the - set; the rows themselves if undirected)
+    const int32_t *perm;                 // candidate rank -> id
     const int64_t *chunk_seg;      // [n_chunks+1] first segment of each lane-chunk
     const int64_t *chunk_cap;      // [n_chunks+1] exclusive prefix of lane-chunk scratch slots (edges)
     int64_t n_chunks;
@@ -64,6 +67,7 @@ struct SampleArgs {
     uint32_t first_sample;
     int64_t n_tasks;               // tasks in the queue
     const int64_t *task_list;      // NULL: task = queue index; else task_list[queue index]
+    int ordered;                   // bipartite / directed: emit (row id, candidate id) as is (R16)
     unsigned long long *task_counter;  // global queue head (zeroed before each launch)
     int2 *edges;                   // scratch (normal) or final array (rerun)
     int32_t *weights;              // ECM

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     uint32_t s_abs[kC];
     // ---- per-chain segment state ----
     bool act[kC];
-    int32_t u[kC], b[kC], cur[kC], id_u[kC];
+    int32_t u[kC], b[kC], cur[kC], id_u[kC], excl[kC];
     uint32_t sg[kC], d[kC], wacc[kC], wwt[kC];
     double xq[kC], dq[kC], h[kC], ku[kC], E[kC], yu[kC], lyu[kC], omT[kC], iomT[kC];
 #pragma unroll
@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         s_abs[c] = 0;
         act[c] = false;
         u[c] = b[c] = cur[c] = id_u[c] = 0;
+        excl[c] = -1;
         sg[c] = d[c] = wacc[c] = wwt[c] = 0;
         xq[c] = 0.0; dq[c] = 1.0; h[c] = 0.0; ku[c] = 0.0; E[c] = 0.0;
         yu[c] = 0.0; lyu[c] = 0.0; omT[c] = 1.0; iomT[c] = 1.0;
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         dq[c] = p2.x;
         ku[c] = p2.y;
         id_u[c] = p3.x;
+        excl[c] = p3.y;  // directed: u's own in-copy (R16), else -1
         if (kModel == FM_ECM) {
             const double2 p4 = *reinterpret_cast<const double2 *>(&r->yu);
             const double2 p5 = *reinterpret_cast<const double2 *>(&r->omT);
@@ -242,7 +244,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         lyv[c] = A.ly_s[cur[c]];
                     }
                     id_v[c] = A.perm[cur[c]];  // issued early; needed only if accepted
-                    landed[c] = true;
+                    // directed: the row's own in-copy is skipped with p = 0, bound kept (R16)
+                    landed[c] = cur[c] != excl[c];
                     w_land[c] = wacc[c];
                     w_wt[c] = wwt[c];
                     d[c]++;
@@ -305,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
 #pragma unroll
         for (int c = 0; c < kC; c++) {
             if (acc[c]) {
-                const int2 ev = make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
+                const int2 ev = A.ordered ? make_int2(id_u[c], id_v[c])
+                                          : make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
                 if (cnt[c] < cap[c]) {
                     A.edges[slot[c] + cnt[c]] = ev;
                     if (kModel == FM_ECM) A.weights[slot[c] + cnt[c]] = w[c];

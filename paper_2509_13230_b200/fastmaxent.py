@@ -25,7 +25,9 @@ FM_OK, FM_ERR_INVALID, FM_ERR_NOMEM, FM_ERR_CUDA, FM_ERR_BOUND, FM_ERR_STATE = 0
 FM_FLAG_WEIGHT_SATURATED, FM_FLAG_SCRATCH_RERUN = 1, 2
 STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ERR_CUDA", -4: "FM_ERR_BOUND",
                 -5: "FM_ERR_STATE"}
-SYMBOLS = ["fm_sort_plan", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
+FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
+_KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
+SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
            "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval"]
 
 
@@ -43,7 +45,7 @@ class _Edges(C.Structure):
 
 
 class _PlanInfo(C.Structure):
-    _fields_ = [("model", C.c_int32), ("n", C.c_int64), ("seg_target", C.c_int64), ("F", C.c_int32),
+    _fields_ = [("model", C.c_int32), ("kind", C.c_int32), ("n_minus", C.c_int64), ("n", C.c_int64), ("seg_target", C.c_int64), ("F", C.c_int32),
                 ("n_segments", C.c_int64), ("n_chunks", C.c_int64), ("est_draws", C.c_int64)]
 
 
@@ -60,6 +62,10 @@ def _load():
     vp, i64, u64 = C.c_void_p, C.c_int64, C.c_uint64
     L.fm_sort_plan.argtypes = [C.c_int, i64, vp, vp, i64, vp, C.POINTER(vp)]
     L.fm_sort_plan.restype = C.c_int
+    L.fm_sort_plan_bipartite.argtypes = [C.c_int, C.c_int, i64, vp, vp, i64, vp, vp, i64, vp, C.POINTER(vp)]
+    L.fm_sort_plan_bipartite.restype = C.c_int
+    L.fm_plan_export_candidates.argtypes = [vp] * 6
+    L.fm_plan_export_candidates.restype = C.c_int
     for f in (L.fm_sample_ubcm, L.fm_sample_ecm):
         f.argtypes = [vp, u64, i64, i64, vp, C.POINTER(_Edges)]
         f.restype = C.c_int
@@ -135,6 +141,8 @@ class Plan:
         info = _PlanInfo()
         _check(lib.fm_plan_get_info(self._h, C.byref(info)))
         self.n = info.n
+        self.kind = info.kind
+        self.n_minus = info.n_minus
         self.seg_target = info.seg_target
         self.F = info.F
         self.n_segments = info.n_segments
@@ -146,12 +154,24 @@ class Plan:
         ecm = self.model == FM_ECM
         keys = ("perm", "kappa_s", "y_s", "ymax", "ly_s", "seg", "seg_h0", "seg_x0", "seg_d0", "seg_omT", "seg_iomT")
         out = {"perm": np.empty(n, np.int32), "kappa_s": np.empty(n, np.float64),
-               "y_s": np.empty(n, np.float64) if ecm else None, "ymax": np.empty(n + 1, np.float64) if ecm else None,
+               "y_s": np.empty(n, np.float64) if ecm else None,
+               "ymax": np.empty(self.n_minus + 1, np.float64) if ecm else None,
                "ly_s": np.empty(n, np.float64) if ecm else None, "seg": np.empty((s, 4), np.int32)}
         for k in keys[6:]:
             out[k] = np.empty(s)
         ptr = lambda a: None if a is None else C.c_void_p(a.ctypes.data)  # noqa: E731
         _check(lib.fm_plan_export(self._h, *(ptr(out[k]) for k in keys)))
+        return out
+
+    def export_candidates(self) -> dict:
+        """fm_plan_export_candidates: the candidate (- / in) set's arrays and the directed exclusions."""
+        nc, n = self.n_minus, self.n
+        ecm = self.model == FM_ECM
+        out = {"cperm": np.empty(nc, np.int32), "ckappa": np.empty(nc), "cy": np.empty(nc) if ecm else None,
+               "cly": np.empty(nc) if ecm else None, "excl": np.empty(n, np.int32)}
+        ptr = lambda a: None if a is None else C.c_void_p(a.ctypes.data)  # noqa: E731
+        _check(lib.fm_plan_export_candidates(self._h, *(ptr(out[k]) for k in ("cperm", "ckappa", "cy", "cly",
+                                                                              "excl"))))
         return out
 
     def free(self):
@@ -243,6 +263,29 @@ def sort_plan(x, y=None, seg_target: int = 256, stream=None) -> Plan:
     h = C.c_void_p()
     _check(lib.fm_sort_plan(model, n, xp, yp, int(seg_target), _stream(stream), C.byref(h)))
     del xk, yk
+    return Plan(h, model)
+
+
+def sort_plan_bipartite(x_plus, x_minus, y_plus=None, y_minus=None, kind: str = "bipartite",
+                        seg_target: int = 256, stream=None) -> Plan:
+    """fm_sort_plan_bipartite: kind "bipartite" (+ set rows vs - set candidates) or
+    "directed" (x_plus/y_plus = out-fitness, x_minus/y_minus = in-fitness, no self loops)."""
+    model = FM_UBCM if y_plus is None else FM_ECM
+    k = _KINDS[kind]
+    p1, k1, n1 = _as_f64(x_plus)
+    p2, k2, n2 = _as_f64(x_minus)
+    q1 = q2 = None
+    keep = []
+    if model == FM_ECM:
+        q1, kk1, ny1 = _as_f64(y_plus)
+        q2, kk2, ny2 = _as_f64(y_minus)
+        keep = [kk1, kk2]
+        if ny1 != n1 or ny2 != n2:
+            raise FastMaxEntError(FM_ERR_INVALID, "y lengths differ from x lengths")
+    h = C.c_void_p()
+    _check(lib.fm_sort_plan_bipartite(model, k, n1, p1, q1, n2, p2, q2, int(seg_target), _stream(stream),
+                                      C.byref(h)))
+    del k1, k2, keep
     return Plan(h, model)
 
 
