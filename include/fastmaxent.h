@@ -120,6 +120,23 @@ fm_status fm_sample_ubcm(const fm_plan *plan, uint64_t seed, int64_t first_sampl
 fm_status fm_sample_ecm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
                         void *cuda_stream, fm_edges *out);
 
+/* Counters of a statistics-mode call (sums over its samples). */
+typedef struct {
+    int64_t draws, landed, accepted;
+    uint32_t flags;
+} fm_counters;
+
+/* Ensemble statistics without edge lists (the consumer of the samples, P:L232-233,
+ * P:L253): draws samples first_sample .. first_sample+n_samples-1 exactly as fm_sample_ubcm/ecm
+ * (same plan, seed and streams, so the same graphs) and ADDS, over those samples, each node's
+ * degree and (ECM) strength into caller-owned DEVICE arrays (uint64, zero them first to start):
+ * undirected: deg_plus[n] (deg_minus/str_minus NULL); bipartite/directed: deg_plus[n] for the
+ * + (out) set and deg_minus[n_minus] for the - (in) set; str_* likewise for the ECM (NULL for
+ * UBCM).  Integer atomics: the sums are deterministic.  Synchronises the stream once. */
+fm_status fm_sample_degrees(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                            void *cuda_stream, uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus,
+                            uint64_t *str_minus, fm_counters *out);
+
 /* Copy a result to caller-owned HOST buffers: edges_host int32[2*n_edges], weights_host
  * int32[n_edges] (may be NULL).  Stream-ordered; synchronises the stream. */
 fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host,

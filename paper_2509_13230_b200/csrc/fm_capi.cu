@@ -615,6 +615,77 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     return FM_OK;
 }
 
+fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                            void *cuda_stream, uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus,
+                            uint64_t *str_minus, fm_counters *out)
+{
+    if (out) memset(out, 0, sizeof(*out));
+    if (!plan_ || !plan_live(plan_)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan_;
+    if (!deg_plus) return fail(FM_ERR_INVALID, "deg_plus is NULL");
+    if (p->kind == FM_UNDIRECTED) {
+        if (deg_minus && deg_minus != deg_plus) return fail(FM_ERR_INVALID, "undirected: deg_minus must be NULL");
+        deg_minus = deg_plus;
+        if (str_minus && str_minus != str_plus) return fail(FM_ERR_INVALID, "undirected: str_minus must be NULL");
+        str_minus = str_plus;
+    } else if (!deg_minus) {
+        return fail(FM_ERR_INVALID, "bipartite/directed: deg_minus is NULL");
+    }
+    if (p->model == FM_ECM && (!str_plus || !str_minus)) return fail(FM_ERR_INVALID, "ECM: strength arrays needed");
+    if (n_samples < 0 || first_sample < 0 || first_sample + n_samples > (int64_t(1) << 32))
+        return fail(FM_ERR_INVALID, "sample range outside [0, 2^32)");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int64_t n_tasks = n_samples * p->n_chunks;
+    if (n_tasks == 0) return FM_OK;
+    Allocs tmp(st);
+    struct Hdr {
+        unsigned long long counters[3];
+        unsigned int flags, pad;
+        unsigned long long task_counter;
+    };
+    Hdr *hd;
+    CK(tmp.get(&hd, 1), "alloc hdr");
+    CK(cudaMemsetAsync(hd, 0, sizeof(Hdr), st), "memset hdr");
+    SampleArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rec = p->rec;
+    a.kappa_s = p->ckappa;
+    a.y_s = p->cy;
+    a.ly_s = p->cly;
+    a.perm = p->cperm;
+    a.ordered = p->kind != FM_UNDIRECTED;
+    a.chunk_seg = p->chunk_seg;
+    a.chunk_cap = p->chunk_cap;
+    a.n_chunks = p->n_chunks;
+    a.key = philox_key(seed);
+    a.first_sample = (uint32_t)first_sample;
+    a.n_tasks = n_tasks;
+    a.task_counter = &hd->task_counter;
+    a.counters = hd->counters;
+    a.flags = &hd->flags;
+    a.deg_row = (unsigned long long *)deg_plus;
+    a.deg_col = (unsigned long long *)deg_minus;
+    a.str_row = (unsigned long long *)str_plus;
+    a.str_col = (unsigned long long *)str_minus;
+    PhaseTimer ts;
+    ts.begin(kPhaseSample, st);
+    CK(launch_sample(p->model, a, st), "sampler launch (degrees)");
+    ts.end(st);
+    Hdr h;
+    unsigned int plan_flags = 0;
+    CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+    CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st), "read flags");
+    CK(cudaStreamSynchronize(st), "sync (degrees)");
+    if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
+    if (out) {
+        out->draws = (int64_t)h.counters[0];
+        out->landed = (int64_t)h.counters[1];
+        out->accepted = (int64_t)h.counters[2];
+        out->flags = (h.flags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u;
+    }
+    return FM_OK;
+}
+
 fm_status fm_sample_ubcm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
                          void *cuda_stream, fm_edges *out)
 {

@@ -80,6 +80,9 @@ struct SampleArgs {
     int64_t *spill_off;            // [n_tasks] spill region of each task: -1 none, -2 failed
     unsigned long long *counters;  // draws, landed, accepted
     unsigned int *flags;
+    // statistics mode (fm_sample_degrees, NEXT-3): when deg_row != NULL no edge list is written;
+    // accepted edges add 1 (and w) to the row node's and the candidate's sums instead
+    unsigned long long *deg_row, *deg_col, *str_row, *str_col;
 };
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st);

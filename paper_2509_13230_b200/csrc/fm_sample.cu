@@ -78,6 +78,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // ---- per-chain segment state ----
     bool act[kC];
     int32_t u[kC], b[kC], cur[kC], id_u[kC], excl[kC];
+    uint32_t row_acc[kC];          // statistics mode: accepted edges of the current segment
+    unsigned long long row_w[kC];  //                  and their weight sum (ECM)
     uint32_t sg[kC], d[kC], wacc[kC], wwt[kC];
     double xq[kC], dq[kC], h[kC], ku[kC], E[kC], yu[kC], lyu[kC], omT[kC], iomT[kC];
 #pragma unroll
@@ -88,6 +90,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         act[c] = false;
         u[c] = b[c] = cur[c] = id_u[c] = 0;
         excl[c] = -1;
+        row_acc[c] = 0;
+        row_w[c] = 0;
         sg[c] = d[c] = wacc[c] = wwt[c] = 0;
         xq[c] = 0.0; dq[c] = 1.0; h[c] = 0.0; ku[c] = 0.0; E[c] = 0.0;
         yu[c] = 0.0; lyu[c] = 0.0; omT[c] = 1.0; iomT[c] = 1.0;
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             fresh[c] = false;
             const bool needc = !act[c];
             if (needc && task[c] >= 0) {
-                if (!A.rerun_base) {
+                if (!A.rerun_base && !A.deg_row) {
                     A.counts[task[c]] = cnt[c];
                     A.spill_off[task[c]] = sp[c];
                 }
@@ -234,6 +238,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 n_draw++;
                 const double R = __ddiv_rn(E[c], h[c]);
                 if (!(R < (double)(b[c] - 1 - cur[c]))) {  // terminal draw (R5)
+                    if (A.deg_row && row_acc[c]) {  // statistics mode: flush the row node's sums
+                        atomicAdd(&A.deg_row[id_u[c]], (unsigned long long)row_acc[c]);
+                        if (kModel == FM_ECM) atomicAdd(&A.str_row[id_u[c]], row_w[c]);
+                        row_acc[c] = 0;
+                        row_w[c] = 0;
+                    }
                     if (g[c] < g_end[c]) start_seg(c, true);
                     else act[c] = false;
                 } else {
@@ -307,7 +317,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         // ---- 6. append accepted edges to the tasks' slots, in draw order ----
 #pragma unroll
         for (int c = 0; c < kC; c++) {
-            if (acc[c]) {
+            if (acc[c] && A.deg_row) {  // statistics mode (NEXT-3): degrees/strengths, no edge list
+                row_acc[c]++;
+                atomicAdd(&A.deg_col[id_v[c]], 1ull);
+                if (kModel == FM_ECM) {
+                    row_w[c] += (unsigned long long)w[c];
+                    atomicAdd(&A.str_col[id_v[c]], (unsigned long long)w[c]);
+                }
+                n_acc++;
+            } else if (acc[c]) {
                 const int2 ev = A.ordered ? make_int2(id_u[c], id_v[c])
                                           : make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
                 if (cnt[c] < cap[c]) {

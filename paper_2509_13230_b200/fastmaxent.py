@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ER
                 -5: "FM_ERR_STATE"}
 FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
 _KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
-SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
+SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
            "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval"]
 
 
@@ -42,6 +42,10 @@ class _Edges(C.Structure):
                 ("edges", C.c_void_p), ("weights", C.c_void_p), ("draws", C.c_int64), ("landed", C.c_int64),
                 ("accepted", C.c_int64), ("segments", C.c_int64), ("chunks", C.c_int64), ("flags", C.c_uint32),
                 ("_owner", C.c_void_p)]
+
+
+class _Counters(C.Structure):
+    _fields_ = [("draws", C.c_int64), ("landed", C.c_int64), ("accepted", C.c_int64), ("flags", C.c_uint32)]
 
 
 class _PlanInfo(C.Structure):
@@ -69,6 +73,8 @@ def _load():
     for f in (L.fm_sample_ubcm, L.fm_sample_ecm):
         f.argtypes = [vp, u64, i64, i64, vp, C.POINTER(_Edges)]
         f.restype = C.c_int
+    L.fm_sample_degrees.argtypes = [vp, u64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Counters)]
+    L.fm_sample_degrees.restype = C.c_int
     L.fm_edges_to_host.argtypes = [C.POINTER(_Edges), vp, vp, vp]
     L.fm_edges_to_host.restype = C.c_int
     L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
@@ -304,6 +310,25 @@ def sample_ubcm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0
 def sample_ecm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None) -> Edges:
     """fm_sample_ecm (Algorithm 1)."""
     return _sample(lib.fm_sample_ecm, plan, seed, n_samples, first_sample, stream)
+
+
+def sample_degrees(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None):
+    """fm_sample_degrees: per-node degree (and ECM strength) sums over the samples, no edge list.
+    Returns (deg_plus, deg_minus, str_plus, str_minus, counters) as CUDA int64 tensors (minus arrays
+    None when undirected; strengths None for the UBCM)."""
+    import torch
+    ecm = plan.model == FM_ECM
+    bip = plan.kind != FM_UNDIRECTED
+    z = lambda n: torch.zeros(n, dtype=torch.int64, device="cuda")  # noqa: E731
+    dp = z(plan.n)
+    dm = z(plan.n_minus) if bip else None
+    sp = z(plan.n) if ecm else None
+    sm = z(plan.n_minus) if (ecm and bip) else None
+    ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
+    c = _Counters()
+    _check(lib.fm_sample_degrees(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
+                                 _stream(stream), ptr(dp), ptr(dm), ptr(sp), ptr(sm), C.byref(c)))
+    return dp, dm, sp, sm, {"draws": c.draws, "landed": c.landed, "accepted": c.accepted, "flags": c.flags}
 
 
 def abi_version() -> int:
