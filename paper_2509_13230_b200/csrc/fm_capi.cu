@@ -1,6 +1,7 @@
 // fm_capi.cu -- the C-ABI (include/fastmaxent.h): validation, stream-ordered memory, launch
 // orchestration of the a1-a6 kernels, status codes.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -167,8 +168,10 @@ void plan_release(Plan *p)
     cudaFree(p->sa.iomT);
     cudaFree(p->ly_s);
     cudaFree(p->rec);
-    cudaFree(p->chunk_seg);
-    cudaFree(p->chunk_cap);
+    for (int k = 0; k < 2; k++) {
+        cudaFree(p->chunk_seg[k]);
+        cudaFree(p->chunk_cap[k]);
+    }
     cudaFree(p->dev_flags);
     p->magic = 0;
     delete p;
@@ -400,32 +403,35 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
         CK(scan_exclusive_i64(seg_work, seg_work, n_seg, work2, wb, st), "scan work");
     }
 
-    // ---- lane-chunking (never changes results) ----
-    const int64_t lane_draws = std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128));
-    const int64_t target = lane_draws * kUnit;
+    // ---- lane-chunking (never changes results): coarse and fine ----
     const int64_t total = h_sc.total_work;
-    p->chunk_target = target;
-    p->n_chunks = std::max<int64_t>(1, (total + target - 1) / target);
-    CK(cudaMallocAsync((void **)&p->chunk_seg, sizeof(int64_t) * (p->n_chunks + 1), st), "alloc chunks");
-    CK(cudaMallocAsync((void **)&p->chunk_cap, sizeof(int64_t) * (p->n_chunks + 1), st), "alloc chunk caps");
-    count_launch();
-    k_chunks<<<grid_for(p->n_chunks, 256), 256, 0, st>>>(n_seg, p->n_chunks, target, seg_work, p->chunk_seg,
-                                                          p->chunk_cap);
-    CK(cudaGetLastError(), "k_chunks");
-    {
-        const size_t cb = scan_tmp_bytes(p->n_chunks + 1);
+    const int64_t lane_draws[2] = {std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128)),
+                                   std::max<int64_t>(1, env_i64("FM_CHUNK_FINE_DRAWS", 64))};
+    const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
+    p->cap_per_sample = 0;
+    for (int k = 0; k < 2; k++) {
+        const int64_t target = lane_draws[k] * kUnit;
+        p->chunk_target[k] = target;
+        const int64_t nch = std::max<int64_t>(1, (total + target - 1) / target);
+        p->n_chunks[k] = nch;
+        CK(cudaMallocAsync((void **)&p->chunk_seg[k], sizeof(int64_t) * (nch + 1), st), "alloc chunks");
+        CK(cudaMallocAsync((void **)&p->chunk_cap[k], sizeof(int64_t) * (nch + 1), st), "alloc chunk caps");
+        count_launch();
+        k_chunks<<<grid_for(nch, 256), 256, 0, st>>>(n_seg, nch, target, seg_work, p->chunk_seg[k], p->chunk_cap[k]);
+        CK(cudaGetLastError(), "k_chunks");
+        const size_t cb = scan_tmp_bytes(nch + 1);
         char *work3;
         CK(tmp.get(&work3, cb), "alloc scan tmp");
-        CK(scan_exclusive_i64(p->chunk_cap, p->chunk_cap, p->n_chunks, work3, cb, st), "scan chunk caps");
-    }
-    // sum over chunks of floor(1.25 w_c / 2^G) + 16 <= floor(1.25 total / 2^G) + 16 n_chunks
-    p->cap_per_sample = ((total + total / 4) >> kG) + 16 * p->n_chunks + 16;
-    const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
-    if (cap_override > 0) {
-        count_launch();
-        k_fill_caps<<<grid_for(p->n_chunks + 1, 256), 256, 0, st>>>(p->chunk_cap, p->n_chunks, cap_override);
-        CK(cudaGetLastError(), "k_fill_caps");
-        p->cap_per_sample = cap_override * p->n_chunks;
+        CK(scan_exclusive_i64(p->chunk_cap[k], p->chunk_cap[k], nch, work3, cb, st), "scan chunk caps");
+        // sum over chunks of floor(1.25 w_c / 2^G) + 16 <= floor(1.25 total / 2^G) + 16 n_chunks
+        int64_t cps = ((total + total / 4) >> kG) + 16 * nch + 16;
+        if (cap_override > 0) {
+            count_launch();
+            k_fill_caps<<<grid_for(nch + 1, 256), 256, 0, st>>>(p->chunk_cap[k], nch, cap_override);
+            CK(cudaGetLastError(), "k_fill_caps");
+            cps = cap_override * nch;
+        }
+        p->cap_per_sample = std::max(p->cap_per_sample, cps);
     }
 
     // the cut invariant (kErrState, impossible for S >= 8) is checked lazily by fm_sample_*: the
@@ -459,6 +465,30 @@ fm_status fm_sort_plan_bipartite(fm_model model, fm_graph kind, int64_t n_plus, 
     }
     return sort_plan_impl(model, kind, n_plus, x_plus, y_plus, n_minus, x_minus, y_minus, seg_target, cuda_stream,
                           plan_out);
+}
+
+// task space of a call: the last K samples use the fine chunks, K covering ~FM_TAIL_FACTOR times
+// the work the resident lanes hold in coarse tasks (so the end of the queue is short tasks)
+static TaskMap make_task_map(const Plan *p, int64_t n_samples, int64_t *n_tasks)
+{
+    TaskMap tm;
+    for (int k = 0; k < 2; k++) {
+        tm.seg[k] = p->chunk_seg[k];
+        tm.cap[k] = p->chunk_cap[k];
+        tm.n_chunks[k] = p->n_chunks[k];
+    }
+    tm.cap_per_sample = p->cap_per_sample;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const double lanes = (double)sms * 768.0;
+    const double tail = (double)env_i64("FM_TAIL_FACTOR", 2) * lanes * (double)(p->chunk_target[0] >> kG);
+    const double per = std::max<double>(1.0, (double)p->est_draws);
+    const int64_t K = std::min<int64_t>(n_samples, (int64_t)std::ceil(tail / per));
+    tm.s_split = n_samples - K;
+    tm.t_split = tm.s_split * tm.n_chunks[0];
+    *n_tasks = tm.t_split + K * tm.n_chunks[1];
+    return tm;
 }
 
 static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
@@ -497,7 +527,8 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     } og{own};
     if (!offsets_h) return fail(FM_ERR_NOMEM, "host offsets");
 
-    const int64_t n_tasks = n_samples * p->n_chunks;
+    int64_t n_tasks = 0;
+    const TaskMap tm = make_task_map(p, n_samples, &n_tasks);
     struct Hdr {
         unsigned long long counters[3];
         unsigned int flags;
@@ -536,10 +567,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.ly_s = p->cly;
         a.perm = p->cperm;
         a.ordered = p->kind != FM_UNDIRECTED;
-        a.chunk_seg = p->chunk_seg;
-        a.chunk_cap = p->chunk_cap;
-        a.n_chunks = p->n_chunks;
-        a.cap_per_sample = p->cap_per_sample;
+        a.tm = tm;
         a.key = philox_key(seed);
         a.first_sample = (uint32_t)first_sample;
         a.n_tasks = n_tasks;
@@ -564,34 +592,53 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             g_sample_launches++;
         }
         CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
-        CK(launch_offsets(n_samples, p->n_chunks, dest, offs_d, st), "offsets");
-        CK(launch_overflow(n_tasks, p->n_chunks, p->chunk_cap, counts, spill_off, &hd->n_overflow, ovl, st),
-           "overflow check");
+        CK(launch_offsets(n_samples, tm, dest, offs_d, st), "offsets");
+        CK(launch_overflow(n_tasks, tm, counts, spill_off, &hd->n_overflow, ovl, st), "overflow check");
+        // The final list is allocated up front with the scratch's capacity (an upper bound unless a
+        // task overflowed both its slot and its spill region), so compaction and the re-run of
+        // overflowed tasks are queued without a host round trip; one synchronisation at the end.
+        int64_t out_cap = slots + spill_cap;
+        auto alloc_out = [&](int64_t cap) -> cudaError_t {
+            cudaError_t e = cudaMallocAsync(&own->edges, sizeof(int2) * std::max<int64_t>(cap, 1), st);
+            if (e == cudaSuccess && model == FM_ECM)
+                e = cudaMallocAsync(&own->weights, sizeof(int32_t) * std::max<int64_t>(cap, 1), st);
+            return e;
+        };
+        auto write_out = [&](int64_t cap) -> cudaError_t {
+            cudaError_t e = launch_compact(cap, n_tasks, tm, counts, dest, spill_off, se, sw, a.spill_e, a.spill_w,
+                                           (int2 *)own->edges, (int32_t *)own->weights, st);
+            if (e != cudaSuccess) return e;
+            SampleArgs r = a;  // deterministic re-run of overflowed tasks straight into the final list
+            r.n_tasks = n_tasks;
+            r.n_tasks_dev = &hd->n_overflow;
+            r.task_list = ovl;
+            r.rerun_base = dest;
+            r.out_cap = cap;
+            r.edges = (int2 *)own->edges;
+            r.weights = (int32_t *)own->weights;
+            return launch_sample(model, r, st);
+        };
+        CK(alloc_out(out_cap), "alloc edges");
+        CK(write_out(out_cap), "compact / rerun");
         CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
            "read offsets");
         CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
         unsigned int plan_flags = 0;
         CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
            "read plan flags");
+        tw.end(st);
         CK(cudaStreamSynchronize(st), "sync (sample)");
         if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
         const int64_t total = offsets_h[n_samples];
-        CK(cudaMallocAsync(&own->edges, sizeof(int2) * std::max<int64_t>(total, 1), st), "alloc edges");
-        if (model == FM_ECM)
-            CK(cudaMallocAsync(&own->weights, sizeof(int32_t) * std::max<int64_t>(total, 1), st), "alloc weights");
-        CK(launch_compact(total, n_tasks, p->n_chunks, p->cap_per_sample, p->chunk_cap, counts, dest, spill_off, se, sw,
-                          a.spill_e, a.spill_w, (int2 *)own->edges, (int32_t *)own->weights, st),
-           "compact");
-        if (h.n_overflow) {  // deterministic re-run of overflowed tasks straight into the final array
-            SampleArgs r = a;
-            r.n_tasks = (int64_t)h.n_overflow;
-            r.task_list = ovl;
-            r.rerun_base = dest;
-            r.edges = (int2 *)own->edges;
-            r.weights = (int32_t *)own->weights;
-            CK(launch_sample(model, r, st), "rerun launch");
+        if (total > out_cap) {  // (pathological overflow) redo the write into an exact-size list
+            cudaFreeAsync(own->edges, st);
+            if (own->weights) cudaFreeAsync(own->weights, st);
+            own->edges = own->weights = nullptr;
+            out_cap = total;
+            CK(alloc_out(out_cap), "alloc edges");
+            CK(write_out(out_cap), "compact / rerun");
+            CK(cudaStreamSynchronize(st), "sync (sample, exact)");
         }
-        tw.end(st);
         out->n_edges = total;
     }
     out->n_samples = n_samples;
@@ -602,7 +649,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     out->landed = (int64_t)h.counters[1];
     out->accepted = (int64_t)h.counters[2];
     out->segments = p->n_seg * n_samples;
-    out->chunks = n_tasks;
+    out->chunks = n_tasks;  // tasks of the call (coarse + fine lane-chunks)
     out->flags = ((h.flags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u) |
                  (h.n_overflow ? FM_FLAG_SCRATCH_RERUN : 0u);
     out->_owner = own;
@@ -635,7 +682,8 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     if (n_samples < 0 || first_sample < 0 || first_sample + n_samples > (int64_t(1) << 32))
         return fail(FM_ERR_INVALID, "sample range outside [0, 2^32)");
     cudaStream_t st = (cudaStream_t)cuda_stream;
-    const int64_t n_tasks = n_samples * p->n_chunks;
+    int64_t n_tasks = 0;
+    const TaskMap tm = make_task_map(p, n_samples, &n_tasks);
     if (n_tasks == 0) return FM_OK;
     Allocs tmp(st);
     struct Hdr {
@@ -654,9 +702,7 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     a.ly_s = p->cly;
     a.perm = p->cperm;
     a.ordered = p->kind != FM_UNDIRECTED;
-    a.chunk_seg = p->chunk_seg;
-    a.chunk_cap = p->chunk_cap;
-    a.n_chunks = p->n_chunks;
+    a.tm = tm;
     a.key = philox_key(seed);
     a.first_sample = (uint32_t)first_sample;
     a.n_tasks = n_tasks;
@@ -730,7 +776,7 @@ fm_status fm_plan_get_info(const fm_plan *plan, fm_plan_info *info)
     info->seg_target = p->S;
     info->F = p->F;
     info->n_segments = p->n_seg;
-    info->n_chunks = p->n_chunks;
+    info->n_chunks = p->n_chunks[0];
     info->est_draws = p->est_draws;
     return FM_OK;
 }

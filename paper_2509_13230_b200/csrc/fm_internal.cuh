@@ -60,10 +60,11 @@ struct Plan {
     SegRec *rec;        // [n_seg] packed copy of the above for the sampler
     int64_t est_draws;  // sum of segment work estimates / 2^G
     // chunking (does not change results)
-    int64_t n_chunks;
-    int64_t *chunk_seg;   // [n_chunks+1] first segment of each lane-chunk
-    int64_t *chunk_cap;   // [n_chunks+1] exclusive prefix of the lane-chunk scratch slots (edges)
-    int64_t chunk_target; // work per lane-chunk (units 2^G)
+    // two chunkings: [0] coarse (most samples), [1] fine (the last samples of a call: short tail)
+    int64_t n_chunks[2];
+    int64_t *chunk_seg[2];   // [n_chunks+1] first segment of each lane-chunk
+    int64_t *chunk_cap[2];   // [n_chunks+1] exclusive prefix of the lane-chunk scratch slots (edges)
+    int64_t chunk_target[2]; // work per lane-chunk (units 2^G)
     int64_t wmax;         // bound of one segment's work (units 2^G)
     int64_t cap_per_sample;  // scratch edges per sample (upper bound of chunk_cap[n_chunks])
     unsigned int *dev_flags; // planner invariant flags (checked by fm_sample_*)

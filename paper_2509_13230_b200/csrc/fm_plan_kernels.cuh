@@ -55,14 +55,37 @@ __global__ void k_pack(int model, int64_t n_seg, SegArrays sa, const double *kap
 // ------------------------------------------------------------------------------------------
 // sampler (fm_sample.cu)
 // ------------------------------------------------------------------------------------------
+// Task space of one fm_sample_* call: samples [0, s_split) use the coarse lane-chunks (index 0),
+// samples [s_split, R) the fine ones (index 1), so the end of the persistent queue consists of
+// short tasks (small end-of-launch tail).  Tasks are numbered sample-major in both ranges, hence
+// in canonical output order.
+struct TaskMap {
+    const int64_t *seg[2];  // chunk_seg of each chunking, [n_chunks + 1]
+    const int64_t *cap[2];  // exclusive prefix of the chunks' scratch slots, [n_chunks + 1]
+    int64_t n_chunks[2];
+    int64_t s_split, t_split;  // t_split = s_split * n_chunks[0]
+    int64_t cap_per_sample;
+};
+
+__device__ __forceinline__ void task_decode(const TaskMap &M, int64_t t, int64_t &s, int64_t &c, int &k)
+{
+    if (t < M.t_split) {
+        k = 0;
+        s = t / M.n_chunks[0];
+        c = t - s * M.n_chunks[0];
+    } else {
+        k = 1;
+        const int64_t t2 = t - M.t_split, s2 = t2 / M.n_chunks[1];
+        s = M.s_split + s2;
+        c = t2 - s2 * M.n_chunks[1];
+    }
+}
+
 struct SampleArgs {
     const SegRec *rec;
     const double *kappa_s, *y_s, *ly_s;  // CANDIDATE arrays (the - set; the rows themselves if undirected)
     const int32_t *perm;                 // candidate rank -> id
-    const int64_t *chunk_seg;      // [n_chunks+1] first segment of each lane-chunk
-    const int64_t *chunk_cap;      // [n_chunks+1] exclusive prefix of lane-chunk scratch slots (edges)
-    int64_t n_chunks;
-    int64_t cap_per_sample;        // scratch edges per sample (>= chunk_cap[n_chunks])
+    TaskMap tm;                    // task -> (sample, chunking, lane-chunk) and scratch slots
     PhiloxKey key;
     uint32_t first_sample;
     int64_t n_tasks;               // tasks in the queue
@@ -72,6 +95,8 @@ struct SampleArgs {
     int2 *edges;                   // scratch (normal) or final array (rerun)
     int32_t *weights;              // ECM
     const int64_t *rerun_base;     // rerun mode: per-task output base (final offsets); NULL otherwise
+    const unsigned long long *n_tasks_dev;  // rerun mode: number of queued tasks, read on the device
+    int64_t out_cap;               // rerun mode: capacity of the final list (writes beyond are dropped)
     int64_t *counts;               // [n_samples * n_chunks] edges produced per task (normal mode)
     int2 *spill_e;                 // spill area for tasks that outgrow their slot (one region of
     int32_t *spill_w;              //   `cap` edges per task, bump-allocated)
@@ -87,15 +112,13 @@ struct SampleArgs {
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st);
 // tasks whose count exceeds their slot -> overflow list (re-run straight into the final array)
-cudaError_t launch_overflow(int64_t n_tasks, int64_t n_chunks, const int64_t *chunk_cap, const int64_t *counts,
-                            const int64_t *spill_off, unsigned long long *n_overflow, int64_t *overflow_list,
-                            cudaStream_t st);
-// gather every task's slot (+ spill) into the final contiguous arrays; host passes the total
-cudaError_t launch_compact(int64_t total, int64_t n_tasks, int64_t n_chunks, int64_t cap_per_sample,
-                           const int64_t *chunk_cap, const int64_t *counts, const int64_t *dest,
+cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *spill_off,
+                            unsigned long long *n_overflow, int64_t *overflow_list, cudaStream_t st);
+// gather every task's slot (+ spill) into the final contiguous arrays of out_cap elements
+cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w, cudaStream_t st);
-cudaError_t launch_offsets(int64_t n_samples, int64_t n_chunks, const int64_t *dest, int64_t *offsets, cudaStream_t st);
+cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets, cudaStream_t st);
 cudaError_t launch_debug_eval(int fn, int64_t n, const double *in, double *out, cudaStream_t st);
 
 }  // namespace fm

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     const SmemLogTab T;
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
+    const int64_t n_tasks = A.n_tasks_dev ? (int64_t)*A.n_tasks_dev : A.n_tasks;
 
     // ---- warp batch of task ids [bpos, bend); lane 0 holds the start of the next batch ----
     unsigned long long next_batch = 0;
@@ -187,18 +188,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     bend = nb + kBatch;
                     if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
                 }
-                if (needc && !warp_done && my < A.n_tasks) {
+                if (needc && !warp_done && my < n_tasks) {
                     const int64_t t = A.task_list ? A.task_list[my] : my;
-                    const int64_t s = t / A.n_chunks, ch = t - s * A.n_chunks;
+                    int64_t s, ch;
+                    int kk;
+                    task_decode(A.tm, t, s, ch, kk);
                     task[c] = t;
-                    g[c] = (int32_t)A.chunk_seg[ch];
-                    g_end[c] = (int32_t)A.chunk_seg[ch + 1];
+                    g[c] = (int32_t)A.tm.seg[kk][ch];
+                    g_end[c] = (int32_t)A.tm.seg[kk][ch + 1];
                     if (A.rerun_base) {
                         slot[c] = A.rerun_base[t];
-                        cap[c] = INT32_MAX;
+                        cap[c] = (int32_t)max((int64_t)0, min((int64_t)INT32_MAX, A.out_cap - slot[c]));  // bounded by the list
                     } else {
-                        slot[c] = s * A.cap_per_sample + A.chunk_cap[ch];
-                        cap[c] = (int32_t)(A.chunk_cap[ch + 1] - A.chunk_cap[ch]);
+                        slot[c] = s * A.tm.cap_per_sample + A.tm.cap[kk][ch];
+                        cap[c] = (int32_t)(A.tm.cap[kk][ch + 1] - A.tm.cap[kk][ch]);
                     }
                     s_abs[c] = A.first_sample + (uint32_t)s;
                     cnt[c] = 0;
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         fresh[c] = true;
                     }
                 }
-                if (bpos >= A.n_tasks) warp_done = true;
+                if (bpos >= n_tasks) warp_done = true;
             }
         }
         bool any_act = false;
@@ -364,17 +367,18 @@ __device__ __forceinline__ bool task_overflowed(int64_t cnt, int64_t cap, int64_
     return cnt > cap && (cnt > 2 * cap || sp < 0);
 }
 
-__global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, int64_t n_chunks, const int64_t *__restrict__ chunk_cap,
-                                                  const int64_t *__restrict__ counts,
+__global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, const TaskMap tm, const int64_t *__restrict__ counts,
                                                   const int64_t *__restrict__ spill_off, unsigned long long *n_overflow,
                                                   int64_t *__restrict__ overflow_list)
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tasks) return;
-    const int64_t c = t % n_chunks;
-    if (task_overflowed(counts[t], chunk_cap[c + 1] - chunk_cap[c], spill_off[t])) {
-        const unsigned long long k = atomicAdd(n_overflow, 1ull);
-        overflow_list[k] = t;
+    int64_t s, c;
+    int k;
+    task_decode(tm, t, s, c, k);
+    if (task_overflowed(counts[t], tm.cap[k][c + 1] - tm.cap[k][c], spill_off[t])) {
+        const unsigned long long o = atomicAdd(n_overflow, 1ull);
+        overflow_list[o] = t;
     }
 }
 
@@ -382,14 +386,14 @@ __global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, int64_t n_chu
 // by one coalesced pass, then each warp copies 32 of the tasks (slot, then spill part),
 // 4 elements per lane in flight.  Overflowed tasks are skipped (re-run into the final array).
 constexpr int kCopyThreads = 256;
-__global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, int64_t n_chunks, int64_t cap_per_sample,
-                                                          const int64_t *__restrict__ chunk_cap,
+__global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const TaskMap tm,
                                                           const int64_t *__restrict__ counts,
                                                           const int64_t *__restrict__ dest,
                                                           const int64_t *__restrict__ spill_off,
                                                           const int2 *__restrict__ se, const int32_t *__restrict__ sw,
                                                           const int2 *__restrict__ spe, const int32_t *__restrict__ spw,
-                                                          int2 *__restrict__ oe, int32_t *__restrict__ ow)
+                                                          int2 *__restrict__ oe, int32_t *__restrict__ ow,
+                                                          int64_t out_cap)
 {
     __shared__ int64_t s_src[kCopyThreads], s_dst[kCopyThreads], s_sp[kCopyThreads];
     __shared__ int32_t s_cnt[kCopyThreads], s_cap[kCopyThreads];
@@ -399,14 +403,17 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, int64
         int32_t cn = 0, cp = 0;
         int64_t src = 0, dst = 0, sp = -1;
         if (t < n_tasks) {
-            const int64_t s = t / n_chunks, c = t - s * n_chunks;
-            const int64_t cap = chunk_cap[c + 1] - chunk_cap[c];
+            int64_t s, c;
+            int k;
+            task_decode(tm, t, s, c, k);
+            const int64_t cap = tm.cap[k][c + 1] - tm.cap[k][c];
             const int64_t cnt = counts[t];
             sp = spill_off[t];
-            cn = task_overflowed(cnt, cap, sp) ? 0 : (int32_t)cnt;
-            cp = (int32_t)cap;
-            src = s * cap_per_sample + chunk_cap[c];
             dst = dest[t];
+            // tasks that would land beyond the list are dropped: the host sees the total and redoes the write
+            cn = task_overflowed(cnt, cap, sp) || dst + cnt > out_cap ? 0 : (int32_t)cnt;
+            cp = (int32_t)cap;
+            src = s * tm.cap_per_sample + tm.cap[k][c];
         }
         s_src[threadIdx.x] = src;
         s_dst[threadIdx.x] = dst;
@@ -454,11 +461,13 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, int64
     }
 }
 
-__global__ void k_offsets(int64_t n_samples, int64_t n_chunks, const int64_t *__restrict__ dest,
+__global__ void k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__restrict__ dest,
                           int64_t *__restrict__ offsets)
 {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s <= n_samples) offsets[s] = dest[s * n_chunks];
+    if (s > n_samples) return;
+    const int64_t t0 = s <= tm.s_split ? s * tm.n_chunks[0] : tm.t_split + (s - tm.s_split) * tm.n_chunks[1];
+    offsets[s] = dest[t0];  // dest[n_tasks] is the total
 }
 
 // diagnostics: fn 0 = fm_log(x), 1 = fm_log1p(x), 2 = -fm_log(u01(k)) with k = (uint32)x
@@ -573,34 +582,31 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
                             : launch_sample_m<FM_ECM>(chains, minb, a, st);
 }
 
-cudaError_t launch_overflow(int64_t n_tasks, int64_t n_chunks, const int64_t *chunk_cap, const int64_t *counts,
-                            const int64_t *spill_off, unsigned long long *n_overflow, int64_t *overflow_list,
-                            cudaStream_t st)
+cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *spill_off,
+                            unsigned long long *n_overflow, int64_t *overflow_list, cudaStream_t st)
 {
     if (n_tasks <= 0) return cudaSuccess;
     count_launch();
-    k_overflow<<<(unsigned)((n_tasks + 255) / 256), 256, 0, st>>>(n_tasks, n_chunks, chunk_cap, counts, spill_off,
-                                                                 n_overflow, overflow_list);
+    k_overflow<<<(unsigned)((n_tasks + 255) / 256), 256, 0, st>>>(n_tasks, tm, counts, spill_off, n_overflow,
+                                                                 overflow_list);
     return cudaGetLastError();
 }
 
-cudaError_t launch_compact(int64_t total, int64_t n_tasks, int64_t n_chunks, int64_t cap_per_sample,
-                           const int64_t *chunk_cap, const int64_t *counts, const int64_t *dest,
+cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w, cudaStream_t st)
 {
-    if (n_tasks <= 0 || total <= 0) return cudaSuccess;
+    if (n_tasks <= 0 || out_cap <= 0) return cudaSuccess;
     count_launch();
     k_compact<<<(unsigned)((n_tasks + kCopyThreads - 1) / kCopyThreads), kCopyThreads, 0, st>>>(
-        n_tasks, n_chunks, cap_per_sample, chunk_cap, counts, dest, spill_off, scratch_e, scratch_w, spill_e, spill_w,
-        out_e, out_w);
+        n_tasks, tm, counts, dest, spill_off, scratch_e, scratch_w, spill_e, spill_w, out_e, out_w, out_cap);
     return cudaGetLastError();
 }
 
-cudaError_t launch_offsets(int64_t n_samples, int64_t n_chunks, const int64_t *dest, int64_t *offsets, cudaStream_t st)
+cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets, cudaStream_t st)
 {
     count_launch();
-    k_offsets<<<(unsigned)((n_samples + 1 + 255) / 256), 256, 0, st>>>(n_samples, n_chunks, dest, offsets);
+    k_offsets<<<(unsigned)((n_samples + 1 + 255) / 256), 256, 0, st>>>(n_samples, tm, dest, offsets);
     return cudaGetLastError();
 }
 
