@@ -31,6 +31,19 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_variant(tag: str, defines: list) -> str:
+    """Experimental build with extra -D flags -> libfastmaxent.<tag>.so (load with FM_LIB_VARIANT=tag)."""
+    global LIB, BUILD, FLAGS
+    saved = LIB, BUILD, FLAGS
+    LIB = os.path.join(HERE, f"libfastmaxent.{tag}.so")
+    BUILD = os.path.join(HERE, f"_build_{tag}")
+    FLAGS = FLAGS + [f"-D{d}" for d in defines]
+    try:
+        return build(force=True)
+    finally:
+        LIB, BUILD, FLAGS = saved
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
@@ -63,4 +76,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:  # python build.py --variant TAG [DEFINE ...]
+        i = sys.argv.index("--variant")
+        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -476,6 +476,7 @@ static TaskMap make_task_map(const Plan *p, int64_t n_samples, int64_t *n_tasks)
         tm.seg[k] = p->chunk_seg[k];
         tm.cap[k] = p->chunk_cap[k];
         tm.n_chunks[k] = p->n_chunks[k];
+        tm.inv_chunks[k] = p->n_chunks[k] > 0 ? 1.0 / (double)p->n_chunks[k] : 0.0;
     }
     tm.cap_per_sample = p->cap_per_sample;
     int dev = 0, sms = 148;
@@ -569,6 +570,8 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.ordered = p->kind != FM_UNDIRECTED;
         a.tm = tm;
         a.key = philox_key(seed);
+        a.lc = log_consts();
+    a.lc = log_consts();
         a.first_sample = (uint32_t)first_sample;
         a.n_tasks = n_tasks;
         a.task_counter = &hd->task_counter;
@@ -704,6 +707,7 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     a.ordered = p->kind != FM_UNDIRECTED;
     a.tm = tm;
     a.key = philox_key(seed);
+    a.lc = log_consts();
     a.first_sample = (uint32_t)first_sample;
     a.n_tasks = n_tasks;
     a.task_counter = &hd->task_counter;

@@ -55,7 +55,7 @@ __device__ __forceinline__ double fm_log_core(double x, double c, const Tab &T)
     const double kd = (double)k;
     const double2 icv = T.ic(i);
     const double invc = icv.x, lc_hi = icv.y, lc_lo = T.lo(i);
-    const LogConsts K = T.C();
+    const LogConsts &K = T.C();
     // r = z * invc - 1 exactly, as r + p_lo
     const double p_hi = __dmul_rn(z, invc);
     const double p_lo = __fma_rn(z, invc, -p_hi);

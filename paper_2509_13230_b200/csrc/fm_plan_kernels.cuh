@@ -2,6 +2,7 @@
 // declared for the host orchestration in fm_capi.cu.
 #pragma once
 #include "fm_internal.cuh"
+#include "fm_math.cuh"
 
 namespace fm {
 
@@ -63,21 +64,35 @@ struct TaskMap {
     const int64_t *seg[2];  // chunk_seg of each chunking, [n_chunks + 1]
     const int64_t *cap[2];  // exclusive prefix of the chunks' scratch slots, [n_chunks + 1]
     int64_t n_chunks[2];
+    double inv_chunks[2];   // 1 / n_chunks (quotient estimate, corrected exactly below)
     int64_t s_split, t_split;  // t_split = s_split * n_chunks[0]
     int64_t cap_per_sample;
 };
+
+// t = s n + c, 0 <= c < n, for t < 2^52: the fp64 quotient estimate is off by at most one
+__device__ __forceinline__ void divmod_est(int64_t t, int64_t n, double inv, int64_t &q, int64_t &r)
+{
+    q = (int64_t)__dmul_rz((double)t, inv);
+    r = t - q * n;
+    if (r < 0) {
+        q--;
+        r += n;
+    } else if (r >= n) {
+        q++;
+        r -= n;
+    }
+}
 
 __device__ __forceinline__ void task_decode(const TaskMap &M, int64_t t, int64_t &s, int64_t &c, int &k)
 {
     if (t < M.t_split) {
         k = 0;
-        s = t / M.n_chunks[0];
-        c = t - s * M.n_chunks[0];
+        divmod_est(t, M.n_chunks[0], M.inv_chunks[0], s, c);
     } else {
         k = 1;
-        const int64_t t2 = t - M.t_split, s2 = t2 / M.n_chunks[1];
+        int64_t s2;
+        divmod_est(t - M.t_split, M.n_chunks[1], M.inv_chunks[1], s2, c);
         s = M.s_split + s2;
-        c = t2 - s2 * M.n_chunks[1];
     }
 }
 
@@ -87,6 +102,7 @@ struct SampleArgs {
     const int32_t *perm;                 // candidate rank -> id
     TaskMap tm;                    // task -> (sample, chunking, lane-chunk) and scratch slots
     PhiloxKey key;
+    LogConsts lc;                  // log polynomial constants (read as parameter-bank operands)
     uint32_t first_sample;
     int64_t n_tasks;               // tasks in the queue
     const int64_t *task_list;      // NULL: task = queue index; else task_list[queue index]

@@ -38,9 +38,14 @@ constexpr int kBatch = 64;  // tasks per warp batch
 __shared__ double2 s_log_ic[kLogTable];
 __shared__ double s_log_lo[kLogTable];
 struct SmemLogTab {
+    const LogConsts &lc;  // in the kernel's parameter bank: constant-bank operands, no register copies
     __device__ __forceinline__ double2 ic(int i) const { return s_log_ic[i]; }
     __device__ __forceinline__ double lo(int i) const { return s_log_lo[i]; }
+#ifdef FM_LOGC_IMM
     __device__ __forceinline__ LogConsts C() const { return log_consts(); }
+#else
+    __device__ __forceinline__ const LogConsts &C() const { return lc; }
+#endif
 };
 
 __device__ __forceinline__ void load_logtab()
@@ -62,7 +67,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
     constexpr int kRecBytes = kModel == FM_ECM ? 96 : 64;  // bytes of SegRec the model reads
     load_logtab();
-    const SmemLogTab T;
+    const SmemLogTab T{A.lc};
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t n_tasks = A.n_tasks_dev ? (int64_t)*A.n_tasks_dev : A.n_tasks;
@@ -221,11 +226,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             if (warp_done) break;
             continue;
         }
-        // ---- 2. first draw of a freshly fetched task ----
-#pragma unroll
-        for (int c = 0; c < kC; c++)
-            if (fresh[c]) E[c] = -fm_log(draw_u(c), T);
-
+        // ---- 2. a freshly fetched task consumes no draw this iteration: like a restarted chain,
+        //      it only computes E of its draw 0 in the convergent block 4+5 ----
         // ---- 3. consume one draw per chain ----
         bool landed[kC];
         uint32_t w_land[kC], w_wt[kC];
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             w_land[c] = w_wt[c] = 0;
             kv[c] = yv[c] = lyv[c] = 0.0;
             id_v[c] = 0;
-            if (act[c]) {
+            if (act[c] && !fresh[c]) {
                 n_draw++;
                 const double R = __ddiv_rn(E[c], h[c]);
                 if (!(R < (double)(b[c] - 1 - cur[c]))) {  // terminal draw (R5)
@@ -472,14 +474,14 @@ __global__ void k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__
 
 // diagnostics: fn 0 = fm_log(x), 1 = fm_log1p(x), 2 = -fm_log(u01(k)) with k = (uint32)x
 __global__ void __launch_bounds__(256) k_debug_eval(int fn, int64_t n, const double *__restrict__ in,
-                                                    double *__restrict__ out)
+                                                    double *__restrict__ out, const LogConsts lc)
 {
     load_logtab();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x = in[i];
     double y;
-    const SmemLogTab T;
+    const SmemLogTab T{lc};
     if (fn == 0) y = fm_log(x, T);
     else if (fn == 1) y = fm_log1p(x, T);
     else y = -fm_log(u01((uint32_t)x), T);
@@ -616,7 +618,7 @@ cudaError_t launch_debug_eval(int fn, int64_t n, const double *in, double *out, 
     if (e != cudaSuccess) return e;
     if (n <= 0) return cudaSuccess;
     count_launch();
-    k_debug_eval<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fn, n, in, out);
+    k_debug_eval<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fn, n, in, out, log_consts());
     return cudaGetLastError();
 }
 

@@ -18,7 +18,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastmaxent.so")
+# FM_LIB_VARIANT=<tag> loads libfastmaxent.<tag>.so (an in-tree experimental build, see build.py)
+LIB_PATH = os.path.join(_HERE, "libfastmaxent.so" if not os.environ.get("FM_LIB_VARIANT")
+                        else f"libfastmaxent.{os.environ['FM_LIB_VARIANT']}.so")
 
 FM_UBCM, FM_ECM = 0, 1
 FM_OK, FM_ERR_INVALID, FM_ERR_NOMEM, FM_ERR_CUDA, FM_ERR_BOUND, FM_ERR_STATE = 0, -1, -2, -3, -4, -5
