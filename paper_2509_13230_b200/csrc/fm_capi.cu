@@ -156,6 +156,7 @@ void plan_release(Plan *p)
         cudaFree(p->cly);
     }
     cudaFree(p->excl);
+    cudaFree(p->cand);
     cudaFree(p->perm);
     cudaFree(p->kappa_s);
     cudaFree(p->y_s);
@@ -344,6 +345,15 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
         count_launch();
         k_excl<<<grid_for(n1, 256), 256, 0, st>>>(n1, p->perm, crank, p->excl);
         CK(cudaGetLastError(), "k_excl");
+    }
+
+    if (model == FM_ECM)
+        CK(cudaMallocAsync((void **)&p->cand, sizeof(double2) * kCandWords(model) * std::max<int64_t>(n2, 1), st),
+           "alloc cand");
+    if (model == FM_ECM && n2 > 0) {
+        count_launch();
+        k_pack_cand<<<grid_for(n2, 256), 256, 0, st>>>((int)model, n2, p->ckappa, p->cperm, p->cy, p->cly, p->cand);
+        CK(cudaGetLastError(), "k_pack_cand");
     }
 
     // ---- a3: suffix max of the candidates' y (beta_min) ----
@@ -567,6 +577,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.y_s = p->cy;
         a.ly_s = p->cly;
         a.perm = p->cperm;
+        a.cand = p->cand;
         a.ordered = p->kind != FM_UNDIRECTED;
         a.tm = tm;
         a.key = philox_key(seed);
@@ -704,6 +715,7 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     a.y_s = p->cy;
     a.ly_s = p->cly;
     a.perm = p->cperm;
+    a.cand = p->cand;
     a.ordered = p->kind != FM_UNDIRECTED;
     a.tm = tm;
     a.key = philox_key(seed);

@@ -37,6 +37,9 @@ struct SegArrays {
     double *h0, *x0, *d0, *omT, *iomT;
 };
 
+// double2 words per candidate in Plan::cand (one 16- or 32-byte record: one L2 sector per gather)
+__host__ __device__ constexpr int kCandWords(int model) { return model == 0 ? 1 : 2; }
+
 struct Plan {
     uint32_t magic;
     int model;
@@ -53,6 +56,8 @@ struct Plan {
     int32_t *cperm;
     double *ckappa, *cy, *cly;
     int32_t *excl;      // [n] directed: candidate rank of each row's own node
+    double2 *cand;      // ECM: [2 nc] the sampler's 32-byte gather record per candidate rank:
+                        //   (kappa, y), (log y, id); id in the low word.  NULL for UBCM
     // a4 segments
     int64_t n_seg;
     SegArrays sa;       // [n_seg] each

@@ -288,6 +288,22 @@ __global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, SegArray
     rec[g] = r;
 }
 
+// the sampler's per-candidate gather record (Plan::cand)
+__global__ void __launch_bounds__(256) k_pack_cand(int model, int64_t nc, const double *__restrict__ ckappa,
+                                                   const int32_t *__restrict__ cperm, const double *__restrict__ cy,
+                                                   const double *__restrict__ cly, double2 *__restrict__ cand)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nc) return;
+    const double id = __hiloint2double(0, cperm[v]);
+    if (model == FM_ECM) {
+        cand[2 * v] = make_double2(ckappa[v], cy[v]);
+        cand[2 * v + 1] = make_double2(cly[v], id);
+    } else {
+        cand[v] = make_double2(ckappa[v], id);
+    }
+}
+
 // test hook (FM_DEBUG_SCRATCH_CAP): every lane-chunk gets the same tiny slot -> forces re-runs
 __global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap)
 {

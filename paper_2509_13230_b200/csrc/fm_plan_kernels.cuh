@@ -50,6 +50,8 @@ __global__ void k_excl(int64_t n, const int32_t *perm, const int32_t *crank, int
 __global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg,
                          int64_t *chunk_cap);
 __global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap);
+__global__ void k_pack_cand(int model, int64_t nc, const double *ckappa, const int32_t *cperm, const double *cy,
+                            const double *cly, double2 *cand);
 __global__ void k_pack(int model, int64_t n_seg, SegArrays sa, const double *kappa_s, const int32_t *perm,
                        const double *y_s, const double *ly_s, const int32_t *excl, SegRec *rec);
 
@@ -100,6 +102,7 @@ struct SampleArgs {
     const SegRec *rec;
     const double *kappa_s, *y_s, *ly_s;  // CANDIDATE arrays (the - set; the rows themselves if undirected)
     const int32_t *perm;                 // candidate rank -> id
+    const double2 *cand;                 // packed gather records (Plan::cand)
     TaskMap tm;                    // task -> (sample, chunking, lane-chunk) and scratch slots
     PhiloxKey key;
     LogConsts lc;                  // log polynomial constants (read as parameter-bank operands)
