@@ -31,17 +31,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_variant(tag: str, defines: list) -> str:
-    """Experimental build with extra -D flags -> libfastmaxent.<tag>.so (load with FM_LIB_VARIANT=tag)."""
-    global LIB, BUILD, FLAGS
-    saved = LIB, BUILD, FLAGS
+def build_variant(tag: str, defines: list, csrc: str = None) -> str:
+    """Experimental build with extra -D flags (and optionally another source tree, e.g. a git
+    revision exported to /tmp) -> libfastmaxent.<tag>.so, loaded with FM_LIB_VARIANT=tag."""
+    global LIB, BUILD, FLAGS, CSRC
+    saved = LIB, BUILD, FLAGS, CSRC
     LIB = os.path.join(HERE, f"libfastmaxent.{tag}.so")
     BUILD = os.path.join(HERE, f"_build_{tag}")
-    FLAGS = FLAGS + [f"-D{d}" for d in defines]
+    if csrc:
+        CSRC = csrc
+    FLAGS = [f if f != saved[3] else CSRC for f in FLAGS] + [f"-D{d}" for d in defines]
     try:
         return build(force=True)
     finally:
-        LIB, BUILD, FLAGS = saved
+        LIB, BUILD, FLAGS, CSRC = saved
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -76,8 +79,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    if "--variant" in sys.argv:  # python build.py --variant TAG [DEFINE ...]
+    if "--variant" in sys.argv:  # python build.py --variant TAG [--csrc DIR] [DEFINE ...]
         i = sys.argv.index("--variant")
-        print(build_variant(sys.argv[i + 1], sys.argv[i + 2:]))
+        rest = sys.argv[i + 2:]
+        src = None
+        if rest[:1] == ["--csrc"]:
+            src, rest = rest[1], rest[2:]
+        print(build_variant(sys.argv[i + 1], rest, src))
     else:
         print(build(force="--force" in sys.argv, verbose=True))

@@ -41,7 +41,8 @@ __host__ __device__ __forceinline__ constexpr LogConsts log_consts()
             0x1.ef35793c76730p-45};
 }
 
-// Tab: accessor with  double2 ic(int i), double lo(int i)  (table)  and  const LogConsts &C()
+// Tab: accessor with  entry(int i, double &invc, double &logc_hi, double &logc_lo)  (table)  and
+// const LogConsts &C()
 
 // log(x) + c * (1/x), x positive, finite, normal; c a tiny correction (|c| <= ulp(x)/2).
 template <bool kCorr, class Tab>
@@ -53,8 +54,8 @@ __device__ __forceinline__ double fm_log_core(double x, double c, const Tab &T)
     const int64_t k = (int64_t)tmp >> 52;
     const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
     const double kd = (double)k;
-    const double2 icv = T.ic(i);
-    const double invc = icv.x, lc_hi = icv.y, lc_lo = T.lo(i);
+    double invc, lc_hi, lc_lo;
+    T.entry(i, invc, lc_hi, lc_lo);
     const LogConsts &K = T.C();
     // r = z * invc - 1 exactly, as r + p_lo
     const double p_hi = __dmul_rn(z, invc);

@@ -34,27 +34,37 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kBatch = 64;  // tasks per warp batch
 
-// per-block copy of the log table (file-scope shared: addressed with constant offsets)
-__shared__ double2 s_log_ic[kLogTable];
-__shared__ double s_log_lo[kLogTable];
+// per-block copy of the log table: (invc, logc_hi) pairs then logc_lo, structure of arrays (a
+// 32-byte array-of-structures entry doubles the bank conflicts of the random lookups)
+struct LogSmem {
+    double2 ic[kLogTable];
+    double lo[kLogTable];
+};
+__shared__ __align__(16) LogSmem s_log;
 struct SmemLogTab {
     const LogConsts &lc;  // in the kernel's parameter bank: constant-bank operands, no register copies
-    __device__ __forceinline__ double2 ic(int i) const { return s_log_ic[i]; }
-    __device__ __forceinline__ double lo(int i) const { return s_log_lo[i]; }
-#ifdef FM_LOGC_IMM
-    __device__ __forceinline__ LogConsts C() const { return log_consts(); }
-#else
+    uint32_t base;        // 32-bit shared address of s_log (opaque: one register, no per-use address math)
+    __device__ __forceinline__ void entry(int i, double &invc, double &hi, double &lo) const
+    {
+        asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(invc), "=d"(hi) : "r"(base + ((uint32_t)i << 4)));
+        asm("ld.shared.f64 %0, [%1+2048];" : "=d"(lo) : "r"(base + ((uint32_t)i << 3)));
+    }
     __device__ __forceinline__ const LogConsts &C() const { return lc; }
-#endif
 };
+static_assert(sizeof(double2) * kLogTable == 2048, "lo offset in SmemLogTab::entry");
 
-__device__ __forceinline__ void load_logtab()
+// fill s_log; returns its shared address, produced after the barrier (so no table read is
+// scheduled before the table is complete)
+__device__ __forceinline__ uint32_t load_logtab()
 {
     for (int j = threadIdx.x; j < kLogTable; j += blockDim.x) {
-        s_log_ic[j] = g_logtab.ic[j];
-        s_log_lo[j] = g_logtab.logc_lo[j];
+        s_log.ic[j] = g_logtab.ic[j];
+        s_log.lo[j] = g_logtab.logc_lo[j];
     }
     __syncthreads();
+    uint32_t base = (uint32_t)__cvta_generic_to_shared(&s_log);
+    asm volatile("mov.b32 %0, %0;" : "+r"(base));
+    return base;
 }
 
 // kC independent chains (lane-chunk tasks) per thread, interleaved for instruction-level
@@ -66,8 +76,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
     constexpr int kRecBytes = kModel == FM_ECM ? 96 : 64;  // bytes of SegRec the model reads
-    load_logtab();
-    const SmemLogTab T{A.lc};
+    const SmemLogTab T{A.lc, load_logtab()};
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t n_tasks = A.n_tasks_dev ? (int64_t)*A.n_tasks_dev : A.n_tasks;
@@ -107,14 +116,36 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
 
     // segment g[c] of chain c's task becomes current (64/96-byte record; the record of the next
     // segment is prefetched into this chain's shared-memory slot with cp.async)
+    // this thread's prefetch slots: 32-bit shared addresses (no generic-address arithmetic)
+    uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(s_dyn) + threadIdx.x * kC * kRecBytes;
+    asm volatile("mov.b32 %0, %0;" : "+r"(slot0));  // opaque: held in a register, not recomputed per use
     auto start_seg = [&](const int c, const bool prefetched) {
-        SegRec *my_next = reinterpret_cast<SegRec *>(s_dyn + (threadIdx.x * kC + c) * kRecBytes);
-        const SegRec *r = prefetched ? my_next : A.rec + g[c];
-        if (prefetched) asm volatile("cp.async.wait_all;\n" ::: "memory");
-        const int4 p0 = *reinterpret_cast<const int4 *>(r);
-        const double2 p1 = *reinterpret_cast<const double2 *>(&r->h0);
-        const double2 p2 = *reinterpret_cast<const double2 *>(&r->d0);
-        const int4 p3 = *reinterpret_cast<const int4 *>(&r->id_u);
+        const uint32_t my_next = slot0 + c * kRecBytes;
+        int4 p0, p3;
+        double2 p1, p2, p4, p5;
+        if (prefetched) {
+            // the slot address passes through the wait: the loads below cannot move above it
+            uint32_t sa = my_next;
+            asm volatile("cp.async.wait_all;\n" : "+r"(sa)::"memory");
+            asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(p0.x), "=r"(p0.y), "=r"(p0.z), "=r"(p0.w) : "r"(sa));
+            asm("ld.shared.v2.f64 {%0,%1}, [%2+16];" : "=d"(p1.x), "=d"(p1.y) : "r"(sa));
+            asm("ld.shared.v2.f64 {%0,%1}, [%2+32];" : "=d"(p2.x), "=d"(p2.y) : "r"(sa));
+            asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4+48];" : "=r"(p3.x), "=r"(p3.y), "=r"(p3.z), "=r"(p3.w) : "r"(sa));
+            if (kModel == FM_ECM) {
+                asm("ld.shared.v2.f64 {%0,%1}, [%2+64];" : "=d"(p4.x), "=d"(p4.y) : "r"(sa));
+                asm("ld.shared.v2.f64 {%0,%1}, [%2+80];" : "=d"(p5.x), "=d"(p5.y) : "r"(sa));
+            }
+        } else {
+            const SegRec *r = A.rec + g[c];
+            p0 = *reinterpret_cast<const int4 *>(r);
+            p1 = *reinterpret_cast<const double2 *>(&r->h0);
+            p2 = *reinterpret_cast<const double2 *>(&r->d0);
+            p3 = *reinterpret_cast<const int4 *>(&r->id_u);
+            if (kModel == FM_ECM) {
+                p4 = *reinterpret_cast<const double2 *>(&r->yu);
+                p5 = *reinterpret_cast<const double2 *>(&r->omT);
+            }
+        }
         u[c] = p0.x;
         cur[c] = p0.y - 1;  // virtual previous position a-1 (R3)
         b[c] = p0.z;
@@ -126,8 +157,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         id_u[c] = p3.x;
         excl[c] = p3.y;  // directed: u's own in-copy (R16), else -1
         if (kModel == FM_ECM) {
-            const double2 p4 = *reinterpret_cast<const double2 *>(&r->yu);
-            const double2 p5 = *reinterpret_cast<const double2 *>(&r->omT);
             yu[c] = p4.x;
             lyu[c] = p4.y;
             omT[c] = p5.x;
@@ -137,12 +166,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         g[c]++;
         act[c] = true;
         if (g[c] < g_end[c]) {
-            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(my_next);
             const char *src = reinterpret_cast<const char *>(A.rec + g[c]);
             constexpr int parts = kModel == FM_ECM ? 6 : 4;
 #pragma unroll
             for (int k = 0; k < parts; k++)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * k), "l"(src + 16 * k)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(my_next + 16 * k), "l"(src + 16 * k)
                              : "memory");
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
@@ -482,12 +510,11 @@ __global__ void k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__
 __global__ void __launch_bounds__(256) k_debug_eval(int fn, int64_t n, const double *__restrict__ in,
                                                     double *__restrict__ out, const LogConsts lc)
 {
-    load_logtab();
+    const SmemLogTab T{lc, load_logtab()};
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x = in[i];
     double y;
-    const SmemLogTab T{lc};
     if (fn == 0) y = fm_log(x, T);
     else if (fn == 1) y = fm_log1p(x, T);
     else y = -fm_log(u01((uint32_t)x), T);
