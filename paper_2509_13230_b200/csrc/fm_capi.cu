@@ -659,9 +659,10 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     out->offsets = offsets_h;
     out->edges = (int32_t *)own->edges;
     out->weights = (int32_t *)own->weights;
+    // every segment ends with exactly one terminal draw; every accepted edge is in the list
     out->draws = (int64_t)h.counters[0];
-    out->landed = (int64_t)h.counters[1];
-    out->accepted = (int64_t)h.counters[2];
+    out->landed = out->draws - p->n_seg * n_samples;
+    out->accepted = out->n_edges;
     out->segments = p->n_seg * n_samples;
     out->chunks = n_tasks;  // tasks of the call (coarse + fine lane-chunks)
     out->flags = ((h.flags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u) |
@@ -741,7 +742,7 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
     if (out) {
         out->draws = (int64_t)h.counters[0];
-        out->landed = (int64_t)h.counters[1];
+        out->landed = out->draws - p->n_seg * n_samples;  // one terminal draw per segment
         out->accepted = (int64_t)h.counters[2];
         out->flags = (h.flags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u;
     }

@@ -68,13 +68,16 @@ __device__ __forceinline__ uint32_t load_logtab()
 }
 
 // kC independent chains (lane-chunk tasks) per thread, interleaved for instruction-level
-// parallelism: with one chain a warp spends most stalls waiting on fixed-latency fp64 / IMAD
-// dependency chains (ncu: "wait"); two independent chains per thread let the scheduler overlap
-// them and amortise the loop / task-management instructions over two draws.
-template <int kModel, int kMinBlocks, int kC>
+// parallelism (instantiated with kC = 1: two chains measured slower, their registers cost more
+// occupancy than their ILP gains).
+// kStats: statistics mode (fm_sample_degrees): degree / strength sums instead of edge lists.
+template <int kModel, int kMinBlocks, int kC, bool kStats>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
+    // rarely used per-chain task state lives in shared memory (registers are the occupancy limit)
+    __shared__ int64_t s_task[kThreads * kC];   // current task id, -1 none
+    __shared__ int64_t s_spill[kThreads * kC];  // its spill region: -1 none, -2 failed
     constexpr int kRecBytes = kModel == FM_ECM ? 96 : 64;  // bytes of SegRec the model reads
     const SmemLogTab T{A.lc, load_logtab()};
     const int lane = threadIdx.x & 31;
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     int64_t bpos = 0, bend = 0;
     bool warp_done = false;
     // ---- per-chain task state ----
-    int64_t task[kC], slot[kC], sp[kC];
+    int64_t slot[kC];
     int32_t g[kC], g_end[kC], cnt[kC], cap[kC];
     uint32_t s_abs[kC];
     // ---- per-chain segment state ----
@@ -99,7 +102,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     double xq[kC], dq[kC], h[kC], ku[kC], E[kC], yu[kC], lyu[kC], omT[kC], iomT[kC];
 #pragma unroll
     for (int c = 0; c < kC; c++) {
-        task[c] = -1; slot[c] = 0; sp[c] = -1;
+        s_task[threadIdx.x * kC + c] = -1;
+        s_spill[threadIdx.x * kC + c] = -1;
+        slot[c] = 0;
         g[c] = g_end[c] = cnt[c] = cap[c] = 0;
         s_abs[c] = 0;
         act[c] = false;
@@ -111,7 +116,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         xq[c] = 0.0; dq[c] = 1.0; h[c] = 0.0; ku[c] = 0.0; E[c] = 0.0;
         yu[c] = 0.0; lyu[c] = 0.0; omT[c] = 1.0; iomT[c] = 1.0;
     }
-    uint32_t n_draw = 0, n_land = 0, n_acc = 0;
+    // draws; landed = draws - segments and accepted = edges are derived by the host (every
+    // segment ends with exactly one terminal draw); statistics mode counts accepted edges
+    uint32_t n_draw = 0, n_acc = 0;
     bool wsat = false;
 
     // segment g[c] of chain c's task becomes current (64/96-byte record; the record of the next
@@ -199,12 +206,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         for (int c = 0; c < kC; c++) {
             fresh[c] = false;
             const bool needc = !act[c];
-            if (needc && task[c] >= 0) {
-                if (!A.rerun_base && !A.deg_row) {
-                    A.counts[task[c]] = cnt[c];
-                    A.spill_off[task[c]] = sp[c];
+            const int ci = threadIdx.x * kC + c;
+            if (needc) {
+                const int64_t tk = s_task[ci];
+                if (tk >= 0) {
+                    if (!A.rerun_base && !kStats) {
+                        A.counts[tk] = cnt[c];
+                        A.spill_off[tk] = s_spill[ci];
+                    }
+                    s_task[ci] = -1;
                 }
-                task[c] = -1;
             }
             const uint32_t nc = __ballot_sync(0xffffffffu, needc && !warp_done);
             if (nc) {
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     int64_t s, ch;
                     int kk;
                     task_decode(A.tm, t, s, ch, kk);
-                    task[c] = t;
+                    s_task[ci] = t;
                     g[c] = (int32_t)A.tm.seg[kk][ch];
                     g_end[c] = (int32_t)A.tm.seg[kk][ch + 1];
                     if (A.rerun_base) {
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     }
                     s_abs[c] = A.first_sample + (uint32_t)s;
                     cnt[c] = 0;
-                    sp[c] = -1;
+                    s_spill[ci] = -1;
                     if (g[c] < g_end[c]) {
                         start_seg(c, false);
                         fresh[c] = true;
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 n_draw++;
                 const double R = __ddiv_rn(E[c], h[c]);
                 if (!(R < (double)(b[c] - 1 - cur[c]))) {  // terminal draw (R5)
-                    if (A.deg_row && row_acc[c]) {  // statistics mode: flush the row node's sums
+                    if (kStats && row_acc[c]) {  // statistics mode: flush the row node's sums
                         atomicAdd(&A.deg_row[id_u[c]], (unsigned long long)row_acc[c]);
                         if (kModel == FM_ECM) atomicAdd(&A.str_row[id_u[c]], row_w[c]);
                         row_acc[c] = 0;
@@ -298,7 +309,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     w_land[c] = wacc[c];
                     w_wt[c] = wwt[c];
                     d[c]++;
-                    n_land++;
                 }
             }
         }
@@ -356,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         // ---- 6. append accepted edges to the tasks' slots, in draw order ----
 #pragma unroll
         for (int c = 0; c < kC; c++) {
-            if (acc[c] && A.deg_row) {  // statistics mode (NEXT-3): degrees/strengths, no edge list
+            if (kStats && acc[c]) {  // statistics mode (NEXT-3): degrees/strengths, no edge list
                 row_acc[c]++;
                 atomicAdd(&A.deg_col[id_v[c]], 1ull);
                 if (kModel == FM_ECM) {
@@ -371,29 +381,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     A.edges[slot[c] + cnt[c]] = ev;
                     if (kModel == FM_ECM) A.weights[slot[c] + cnt[c]] = w[c];
                 } else if (!A.rerun_base && cnt[c] < 2 * cap[c]) {  // spill: one extra region of `cap`
-                    if (sp[c] == -1) {
+                    const int ci = threadIdx.x * kC + c;
+                    int64_t sp = s_spill[ci];
+                    if (sp == -1) {
                         const unsigned long long o = atomicAdd(A.spill_counter, (unsigned long long)cap[c]);
-                        sp[c] = (int64_t)(o + cap[c]) <= A.spill_cap ? (int64_t)o : -2;
+                        sp = (int64_t)(o + cap[c]) <= A.spill_cap ? (int64_t)o : -2;
+                        s_spill[ci] = sp;
                     }
-                    if (sp[c] >= 0) {
-                        A.spill_e[sp[c] + cnt[c] - cap[c]] = ev;
-                        if (kModel == FM_ECM) A.spill_w[sp[c] + cnt[c] - cap[c]] = w[c];
+                    if (sp >= 0) {
+                        A.spill_e[sp + cnt[c] - cap[c]] = ev;
+                        if (kModel == FM_ECM) A.spill_w[sp + cnt[c] - cap[c]] = w[c];
                     }
                 }
                 cnt[c]++;
-                n_acc++;
             }
         }
     }
     if (A.rerun_base) return;
     const unsigned dr = __reduce_add_sync(0xffffffffu, n_draw);
-    const unsigned la = __reduce_add_sync(0xffffffffu, n_land);
     const unsigned ac = __reduce_add_sync(0xffffffffu, n_acc);
     const bool anysat = __any_sync(0xffffffffu, wsat);
     if (lane == 0) {
         atomicAdd(&A.counters[0], (unsigned long long)dr);
-        atomicAdd(&A.counters[1], (unsigned long long)la);
-        atomicAdd(&A.counters[2], (unsigned long long)ac);
+        if (kStats) atomicAdd(&A.counters[2], (unsigned long long)ac);
         if (anysat) atomicOr(A.flags, kFlagWeightSat);
     }
 }
@@ -560,7 +570,7 @@ cudaError_t ensure_log_table(cudaStream_t st)
 
 // the sampler is instantiated for several register budgets (min resident blocks per SM);
 // FM_SAMPLE_MINB selects one at run time (tuning), default per model
-template <int kModel, int kMinB, int kC>
+template <int kModel, int kMinB, int kC, bool kStats>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
     int dev = 0, sms = 0, per = 0;
@@ -569,32 +579,28 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
     const size_t dyn = (size_t)kThreads * kC * (kModel == FM_ECM ? 96 : 64);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaFuncSetAttribute(k_sample<kModel, kMinB, kC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dyn);
         attr_set = true;
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC>, kThreads, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC, kStats>, kThreads, dyn);
     int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
     const int64_t need = (a.n_tasks + kThreads * kC - 1) / (kThreads * kC);  // <= one task per chain at start
     if (need < blocks) blocks = need;
     count_launch();
-    k_sample<kModel, kMinB, kC><<<(unsigned)blocks, kThreads, dyn, st>>>(a);
+    k_sample<kModel, kMinB, kC, kStats><<<(unsigned)blocks, kThreads, dyn, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int kModel>
-static cudaError_t launch_sample_m(int chains, int minb, const SampleArgs &a, cudaStream_t st)
+// one chain per thread (kC = 2 measured slower: register-limited occupancy); FM_SAMPLE_MINB
+// overrides the blocks-per-SM target of the register budget (tuning experiments)
+template <int kModel, bool kStats>
+static cudaError_t launch_sample_m(int minb, const SampleArgs &a, cudaStream_t st)
 {
-    if (chains == 2) {
-        switch (minb) {
-        case 1: return launch_sample_t<kModel, 1, 2>(a, st);
-        case 3: return launch_sample_t<kModel, 3, 2>(a, st);
-        default: return launch_sample_t<kModel, 2, 2>(a, st);
-        }
-    }
     switch (minb) {
-    case 2: return launch_sample_t<kModel, 2, 1>(a, st);
-    case 4: return launch_sample_t<kModel, 4, 1>(a, st);
-    default: return launch_sample_t<kModel, 3, 1>(a, st);
+    case 2: return launch_sample_t<kModel, 2, 1, kStats>(a, st);
+    case 4: return launch_sample_t<kModel, 4, 1, kStats>(a, st);
+    default: return launch_sample_t<kModel, 3, 1, kStats>(a, st);
     }
 }
 
@@ -610,11 +616,11 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
         if (e != cudaSuccess) return e;
     }
     const char *ev = getenv("FM_SAMPLE_MINB");
-    const char *ec = getenv("FM_SAMPLE_CHAINS");
-    const int chains = ec && *ec ? atoi(ec) : 1;
-    const int minb = ev && *ev ? atoi(ev) : (chains == 2 ? 2 : (model == FM_UBCM ? 3 : 2));
-    return model == FM_UBCM ? launch_sample_m<FM_UBCM>(chains, minb, a, st)
-                            : launch_sample_m<FM_ECM>(chains, minb, a, st);
+    const int minb = ev && *ev ? atoi(ev) : 3;  // 24 warps/SM (measured best for both models)
+    const bool stats = a.deg_row != nullptr;
+    if (model == FM_UBCM)
+        return stats ? launch_sample_m<FM_UBCM, true>(minb, a, st) : launch_sample_m<FM_UBCM, false>(minb, a, st);
+    return stats ? launch_sample_m<FM_ECM, true>(minb, a, st) : launch_sample_m<FM_ECM, false>(minb, a, st);
 }
 
 cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *spill_off,
