@@ -276,8 +276,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         for (int c = 0; c < kC; c++) {
             landed[c] = false;
             w_land[c] = w_wt[c] = 0;
-            kv[c] = yv[c] = lyv[c] = 0.0;
-            id_v[c] = 0;
+            // kv and id_v are left undefined unless the draw lands: a defined "else" value makes
+            // the compiler copy the gathered register at the branch merge, i.e. wait for the
+            // gather there instead of at its first use (ncu: long-scoreboard stall).  ECM keeps
+            // them defined: undefined (or gathered after the merge) they cost a register spill
+            // at 24 warps/SM and measured slower
+            if (kModel == FM_ECM) {
+                kv[c] = yv[c] = lyv[c] = 0.0;
+                id_v[c] = 0;
+            }
             if (act[c] && !fresh[c]) {
                 n_draw++;
                 const double R = __ddiv_rn(E[c], h[c]);
@@ -326,10 +333,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 // (kv + 0*us) orders the use of the gathered kv after the Philox rounds above, so
                 // the gather latency hides behind them while the two logarithms below (E of the
                 // next draw, log1p of this candidate) stay independent; exact since us in (0,1)
-                const double kvd = __dadd_rn(kv[c], __dmul_rn(us, 0.0));
+                // (kv is read only if landed: the ?: evaluates the selected operand only)
                 const double Enew = -fm_log(us, T);
                 if (kModel == FM_UBCM) {
-                    const double X = landed[c] ? __dmul_rn(ku[c], kvd) : 1.0;
+                    const double X = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(us, 0.0))) : 1.0;
                     const double D = __dadd_rn(1.0, X);
                     const double hn = fm_log1p(X, T);
                     if (landed[c]) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
@@ -339,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         h[c] = hn;
                     }
                 } else {
-                    const double z = landed[c] ? __dmul_rn(ku[c], kvd) : 1.0;
-                    const double t = __dmul_rn(yu[c], yv[c]);
+                    const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(us, 0.0))) : 1.0;
+                    const double t = __dmul_rn(yu[c], yv[c]);  // (ECM: yv defined on every path, see above)
                     const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
                     const double hn = fm_log1p(__dmul_rn(z, iomT[c]), T);
                     if (landed[c]) {
