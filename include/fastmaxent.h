@@ -137,6 +137,16 @@ fm_status fm_sample_degrees(const fm_plan *plan, uint64_t seed, int64_t first_sa
                             void *cuda_stream, uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus,
                             uint64_t *str_minus, fm_counters *out);
 
+/* Rich-club profile of the ensemble (the top-alpha density of P:L58-60):
+ * draws the same samples as fm_sample_ubcm/ecm (undirected plans only, else FM_ERR_STATE) and
+ * ADDS to the caller-owned DEVICE array e_top[n+1] (uint64; zero it first to start), for every
+ * m = 0..n, the number of sampled edges joining two of the m top-ranked nodes, summed over the
+ * samples.  Ranks are the plan's sort order (kappa descending, ties by id; fm_plan_export's perm):
+ * for the UBCM the order of expected degree.  Density of the top m: e_top[m] / (R m(m-1)/2).
+ * Integer atomics: deterministic.  Synchronises the stream once. */
+fm_status fm_sample_richclub(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                             void *cuda_stream, uint64_t *e_top, fm_counters *out);
+
 /* Copy a result to caller-owned HOST buffers: edges_host int32[2*n_edges], weights_host
  * int32[n_edges] (may be NULL).  Stream-ordered; synchronises the stream. */
 fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host,

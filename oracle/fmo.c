@@ -870,3 +870,44 @@ double fmo_expected_edges(int model, int64_t n, const double *x, const double *y
     free(E.rowsum);
     return tot;
 }
+
+/* ---- rich club: density of edges among the top-m nodes, P:L58-60, P:L233 ----
+ * The top m nodes are the first m of a given order (rank -> node id `order`).
+ * fmo_richclub_count: e_top[m] = #{edges (i,j) of the list : rank(i) < m and rank(j) < m}, m = 0..n,
+ *   straight from the definition: an edge is inside the top m iff its larger endpoint rank is < m.
+ * fmo_expected_richclub: E[e_top[m]] = sum over pairs of top-m nodes of p_ij, and the variance
+ *   sum p_ij (1 - p_ij) (independent edges), m = 0..n, adding one node at a time. */
+void fmo_richclub_count(int64_t n, const int32_t *order, int64_t n_edges, const int32_t *edges, int64_t *e_top)
+{
+    int64_t *rank = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *hist = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t r = 0; r < n; r++) rank[order[r]] = r;
+    for (int64_t e = 0; e < n_edges; e++) {
+        int64_t a = rank[edges[2 * e]], b = rank[edges[2 * e + 1]];
+        hist[a > b ? a : b]++;
+    }
+    e_top[0] = 0;
+    for (int64_t m = 0; m < n; m++) e_top[m + 1] = e_top[m] + hist[m];
+    free(rank);
+    free(hist);
+}
+
+void fmo_expected_richclub(int model, int64_t n, const double *x, const double *y, const int32_t *order,
+                           double *mean, double *var)
+{
+    mean[0] = 0.0;
+    var[0] = 0.0;
+    for (int64_t m = 0; m < n; m++) {
+        int64_t j = order[m];
+        double add = 0.0, addv = 0.0;
+        for (int64_t r = 0; r < m; r++) {
+            int64_t i = order[r];
+            double t;
+            double pij = pair_p(model, x[i], x[j], model == FMO_ECM ? y[i] : 0.0, model == FMO_ECM ? y[j] : 0.0, &t);
+            add += pij;
+            addv += pij * (1.0 - pij);
+        }
+        mean[m + 1] = mean[m] + add;
+        var[m + 1] = var[m] + addv;
+    }
+}

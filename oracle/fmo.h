@@ -86,6 +86,11 @@ void fmo_result_free(fmo_result *r);
  * ECM z/(1 - t + z), z = x_i x_j y_i y_j, t = y_i y_j.  s/svar may be NULL for UBCM. */
 void fmo_expected(int model, int64_t n, const double *x, const double *y, const int32_t *nodes,
                   int64_t n_nodes, int nthreads, double *k, double *kvar, double *s, double *svar);
+/* rich club: e_top[m] = edges among the first m nodes of `order` (rank -> id), m = 0..n;
+ * and its expectation / variance under the model (independent pairs) */
+void fmo_richclub_count(int64_t n, const int32_t *order, int64_t n_edges, const int32_t *edges, int64_t *e_top);
+void fmo_expected_richclub(int model, int64_t n, const double *x, const double *y, const int32_t *order,
+                           double *mean, double *var);
 /* sum_{i<j} p_ij exactly, O(N^2), threaded */
 double fmo_expected_edges(int model, int64_t n, const double *x, const double *y, int nthreads);
 

@@ -99,6 +99,10 @@ def lib():
     L.fmo_expected.restype = None
     L.fmo_expected_edges.argtypes = [C.c_int, C.c_int64, f64p, f64p, C.c_int]
     L.fmo_expected_edges.restype = C.c_double
+    L.fmo_richclub_count.argtypes = [C.c_int64, i32p, C.c_int64, i32p, i64p]
+    L.fmo_richclub_count.restype = None
+    L.fmo_expected_richclub.argtypes = [C.c_int, C.c_int64, f64p, f64p, i32p, f64p, f64p]
+    L.fmo_expected_richclub.restype = None
     _lib = L
     return L
 
@@ -331,6 +335,29 @@ def expected_edges(x, y=None, nthreads: int | None = None) -> float:
     model = UBCM if y is None else ECM
     yy = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
     return lib().fmo_expected_edges(model, len(x), _p(x, C.c_double), _p(yy, C.c_double), int(nthreads or ncores()))
+
+
+def richclub_count(order, edges) -> np.ndarray:
+    """Rich club: e_top[m] = edges of the list among the first m nodes of ``order``
+    (rank -> node id), m = 0..n (fmo_richclub_count)."""
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+    out = np.empty(len(order) + 1, dtype=np.int64)
+    lib().fmo_richclub_count(len(order), _p(order, C.c_int32), len(e), _p(e, C.c_int32), _p(out, C.c_int64))
+    return out
+
+
+def expected_richclub(x, y, order):
+    """E[e_top[m]] and Var[e_top[m]], m = 0..n, for the top-m nodes of ``order`` (independent pairs,
+    P:L90-93; fmo_expected_richclub, O(n^2))."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    model = UBCM if y is None else ECM
+    yy = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    mean, var = np.empty(len(order) + 1), np.empty(len(order) + 1)
+    lib().fmo_expected_richclub(model, len(x), _p(x, C.c_double), _p(yy, C.c_double), _p(order, C.c_int32),
+                                _p(mean, C.c_double), _p(var, C.c_double))
+    return mean, var
 
 
 def expected_edges_binned(x, y=None, ratio: float = 1.003) -> float:

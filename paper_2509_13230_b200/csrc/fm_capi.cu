@@ -677,6 +677,11 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     return FM_OK;
 }
 
+// statistics-mode sampler launch shared by fm_sample_degrees and fm_sample_richclub
+static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, int64_t n_samples, cudaStream_t st,
+                            uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus, uint64_t *str_minus,
+                            uint64_t *rank_hist, fm_counters *out);
+
 fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
                             void *cuda_stream, uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus,
                             uint64_t *str_minus, fm_counters *out)
@@ -696,7 +701,42 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     if (p->model == FM_ECM && (!str_plus || !str_minus)) return fail(FM_ERR_INVALID, "ECM: strength arrays needed");
     if (n_samples < 0 || first_sample < 0 || first_sample + n_samples > (int64_t(1) << 32))
         return fail(FM_ERR_INVALID, "sample range outside [0, 2^32)");
+    return stats_impl(p, seed, first_sample, n_samples, (cudaStream_t)cuda_stream, deg_plus, deg_minus, str_plus,
+                      str_minus, nullptr, out);
+}
+
+fm_status fm_sample_richclub(const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                             void *cuda_stream, uint64_t *e_top, fm_counters *out)
+{
+    if (out) memset(out, 0, sizeof(*out));
+    if (!plan_ || !plan_live(plan_)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan_;
+    if (p->kind != FM_UNDIRECTED) return fail(FM_ERR_STATE, "rich club: undirected plans only");
+    if (!e_top) return fail(FM_ERR_INVALID, "e_top is NULL");
+    if (n_samples < 0 || first_sample < 0 || first_sample + n_samples > (int64_t(1) << 32))
+        return fail(FM_ERR_INVALID, "sample range outside [0, 2^32)");
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    Allocs tmp(st);
+    uint64_t *hist, *cum;
+    char *work;
+    const size_t sb = scan_tmp_bytes(p->n + 1);
+    CK(tmp.get(&hist, p->n + 1), "alloc rank histogram");
+    CK(tmp.get(&cum, p->n + 1), "alloc rank prefix");
+    CK(tmp.get(&work, sb), "alloc scan tmp");
+    CK(cudaMemsetAsync(hist, 0, sizeof(uint64_t) * (p->n + 1), st), "memset histogram");
+    fm_status r = stats_impl(p, seed, first_sample, n_samples, st, nullptr, nullptr, nullptr, nullptr, hist, out);
+    if (r != FM_OK) return r;
+    // e_top[m] += sum_{r < m} hist[r]: edges whose larger rank is below m join two top-m nodes
+    CK(scan_exclusive_u64(hist, cum, p->n, work, sb, st), "scan histogram");
+    CK(launch_add_u64(cum, e_top, p->n + 1, st), "accumulate e_top");
+    CK(cudaStreamSynchronize(st), "sync (rich club)");
+    return FM_OK;
+}
+
+static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, int64_t n_samples, cudaStream_t st,
+                            uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus, uint64_t *str_minus,
+                            uint64_t *rank_hist, fm_counters *out)
+{
     int64_t n_tasks = 0;
     const TaskMap tm = make_task_map(p, n_samples, &n_tasks);
     if (n_tasks == 0) return FM_OK;
@@ -730,6 +770,7 @@ fm_status fm_sample_degrees(const fm_plan *plan_, uint64_t seed, int64_t first_s
     a.deg_col = (unsigned long long *)deg_minus;
     a.str_row = (unsigned long long *)str_plus;
     a.str_col = (unsigned long long *)str_minus;
+    a.rank_hist = (unsigned long long *)rank_hist;
     PhaseTimer ts;
     ts.begin(kPhaseSample, st);
     CK(launch_sample(p->model, a, st), "sampler launch (degrees)");

@@ -127,6 +127,8 @@ struct SampleArgs {
     // statistics mode (fm_sample_degrees, NEXT-3): when deg_row != NULL no edge list is written;
     // accepted edges add 1 (and w) to the row node's and the candidate's sums instead
     unsigned long long *deg_row, *deg_col, *str_row, *str_col;
+    // rich club (statistics mode, undirected): accepted edges counted by their larger rank
+    unsigned long long *rank_hist;
 };
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st);
@@ -138,6 +140,8 @@ cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, 
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w, cudaStream_t st);
 cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets, cudaStream_t st);
+// out[i] += in[i], i < n (uint64)
+cudaError_t launch_add_u64(const uint64_t *in, uint64_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_debug_eval(int fn, int64_t n, const double *in, double *out, cudaStream_t st);
 
 }  // namespace fm

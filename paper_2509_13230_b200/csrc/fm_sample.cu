@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 n_draw++;
                 const double R = __ddiv_rn(E[c], h[c]);
                 if (!(R < (double)(b[c] - 1 - cur[c]))) {  // terminal draw (R5)
-                    if (kStats && row_acc[c]) {  // statistics mode: flush the row node's sums
+                    if (kStats && row_acc[c] && A.deg_row) {  // statistics mode: flush the row node's sums
                         atomicAdd(&A.deg_row[id_u[c]], (unsigned long long)row_acc[c]);
                         if (kModel == FM_ECM) atomicAdd(&A.str_row[id_u[c]], row_w[c]);
                         row_acc[c] = 0;
@@ -374,12 +374,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
 #pragma unroll
         for (int c = 0; c < kC; c++) {
             if (kStats && acc[c]) {  // statistics mode (NEXT-3): degrees/strengths, no edge list
-                row_acc[c]++;
-                atomicAdd(&A.deg_col[id_v[c]], 1ull);
-                if (kModel == FM_ECM) {
-                    row_w[c] += (unsigned long long)w[c];
-                    atomicAdd(&A.str_col[id_v[c]], (unsigned long long)w[c]);
+                if (A.deg_row) {
+                    row_acc[c]++;
+                    atomicAdd(&A.deg_col[id_v[c]], 1ull);
+                    if (kModel == FM_ECM) {
+                        row_w[c] += (unsigned long long)w[c];
+                        atomicAdd(&A.str_col[id_v[c]], (unsigned long long)w[c]);
+                    }
                 }
+                // rich club: the edge lies within the top-m nodes iff its larger rank cur < m
+                if (A.rank_hist) atomicAdd(&A.rank_hist[cur[c]], 1ull);
                 n_acc++;
             } else if (acc[c]) {
                 const int2 ev = A.ordered ? make_int2(id_u[c], id_v[c])
@@ -523,6 +527,12 @@ __global__ void k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__
     offsets[s] = dest[t0];  // dest[n_tasks] is the total
 }
 
+__global__ void k_add_u64(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, int64_t n)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] += in[i];
+}
+
 // diagnostics: fn 0 = fm_log(x), 1 = fm_log1p(x), 2 = -fm_log(u01(k)) with k = (uint32)x
 __global__ void __launch_bounds__(256) k_debug_eval(int fn, int64_t n, const double *__restrict__ in,
                                                     double *__restrict__ out, const LogConsts lc)
@@ -588,6 +598,13 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
     if (!attr_set) {
         cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dyn);
+        // shared-memory carveout (percent of the unified L1/shared capacity): the driver's default
+        // picked 135 KB of shared memory for 3 x 27 KB of need; a smaller carveout leaves more L1
+        // for the kappa / perm gathers (FM_SAMPLE_CARVEOUT overrides; -1 = driver default)
+        const char *cv = getenv("FM_SAMPLE_CARVEOUT");
+        const int carve = cv && *cv ? atoi(cv) : -1;
+        if (carve >= 0) cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>,
+                                             cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         attr_set = true;
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC, kStats>, kThreads, dyn);
@@ -624,7 +641,7 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
     }
     const char *ev = getenv("FM_SAMPLE_MINB");
     const int minb = ev && *ev ? atoi(ev) : 3;  // 24 warps/SM (measured best for both models)
-    const bool stats = a.deg_row != nullptr;
+    const bool stats = a.deg_row != nullptr || a.rank_hist != nullptr;
     if (model == FM_UBCM)
         return stats ? launch_sample_m<FM_UBCM, true>(minb, a, st) : launch_sample_m<FM_UBCM, false>(minb, a, st);
     return stats ? launch_sample_m<FM_ECM, true>(minb, a, st) : launch_sample_m<FM_ECM, false>(minb, a, st);
@@ -655,6 +672,14 @@ cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *
 {
     count_launch();
     k_offsets<<<(unsigned)((n_samples + 1 + 255) / 256), 256, 0, st>>>(n_samples, tm, dest, offsets);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_add_u64(const uint64_t *in, uint64_t *out, int64_t n, cudaStream_t st)
+{
+    if (n <= 0) return cudaSuccess;
+    count_launch();
+    k_add_u64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, n);
     return cudaGetLastError();
 }
 

@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ER
                 -5: "FM_ERR_STATE"}
 FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
 _KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
-SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
+SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
            "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval"]
 
 
@@ -77,6 +77,8 @@ def _load():
         f.restype = C.c_int
     L.fm_sample_degrees.argtypes = [vp, u64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Counters)]
     L.fm_sample_degrees.restype = C.c_int
+    L.fm_sample_richclub.argtypes = [vp, u64, i64, i64, vp, vp, C.POINTER(_Counters)]
+    L.fm_sample_richclub.restype = C.c_int
     L.fm_edges_to_host.argtypes = [C.POINTER(_Edges), vp, vp, vp]
     L.fm_edges_to_host.restype = C.c_int
     L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
@@ -331,6 +333,17 @@ def sample_degrees(plan: Plan, seed: int, n_samples: int = 1, first_sample: int 
     _check(lib.fm_sample_degrees(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
                                  _stream(stream), ptr(dp), ptr(dm), ptr(sp), ptr(sm), C.byref(c)))
     return dp, dm, sp, sm, {"draws": c.draws, "landed": c.landed, "accepted": c.accepted, "flags": c.flags}
+
+
+def sample_richclub(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None):
+    """fm_sample_richclub: e_top[m] = edges among the m top-ranked nodes (plan order), summed over
+    the samples, m = 0..n, as a CUDA int64 tensor; plus the counters.  Undirected plans only."""
+    import torch
+    e = torch.zeros(plan.n + 1, dtype=torch.int64, device="cuda")
+    c = _Counters()
+    _check(lib.fm_sample_richclub(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
+                                  _stream(stream), C.c_void_p(e.data_ptr()), C.byref(c)))
+    return e, {"draws": c.draws, "landed": c.landed, "accepted": c.accepted, "flags": c.flags}
 
 
 def abi_version() -> int:
