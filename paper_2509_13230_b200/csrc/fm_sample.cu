@@ -599,10 +599,11 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dyn);
         // shared-memory carveout (percent of the unified L1/shared capacity): the driver's default
-        // picked 135 KB of shared memory for 3 x 27 KB of need; a smaller carveout leaves more L1
-        // for the kappa / perm gathers (FM_SAMPLE_CARVEOUT overrides; -1 = driver default)
+        // picked 135 KB of shared memory for 3 x 27 KB of need; 40 % leaves more L1 for the kappa /
+        // perm gathers (UBCM kernel -1 %; 0 % starves occupancy: +70 %).  FM_SAMPLE_CARVEOUT
+        // overrides (-1 = driver default)
         const char *cv = getenv("FM_SAMPLE_CARVEOUT");
-        const int carve = cv && *cv ? atoi(cv) : -1;
+        const int carve = cv && *cv ? atoi(cv) : 40;
         if (carve >= 0) cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         attr_set = true;
