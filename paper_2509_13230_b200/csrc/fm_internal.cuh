@@ -127,8 +127,17 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
     return c;
 }
 
-// u01(k) = (k + 0.5) 2^-32 (R2); both operations exact
+// u01(k) = (k + 0.5) 2^-32 (R2); every operation exact.  The word is placed in the
+// mantissa of 2^52 (v = 2^52 + k, no conversion instruction: the I2F conversions are
+// variable-latency and compete for the six dependency scoreboards with the gathers), then
+// v - (2^52 - 1/2) = k + 1/2 exactly (Sterbenz) and the scale is a power of two.
 __device__ __forceinline__ double u01(uint32_t k)
+{
+    return __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, (int)k), 0x1p52 - 0.5), 0x1p-32);
+}
+// the same value through a conversion instruction (the ECM sampler: measured faster there, the
+// form above costs it a register spill)
+__device__ __forceinline__ double u01_cvt(uint32_t k)
 {
     return __dmul_rn(__dadd_rn((double)k, 0.5), 0x1p-32);
 }

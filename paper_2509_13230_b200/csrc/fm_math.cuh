@@ -53,7 +53,8 @@ __device__ __forceinline__ double fm_log_core(double x, double c, const Tab &T)
     const int i = (int)((tmp >> 45) & (kLogTable - 1));
     const int64_t k = (int64_t)tmp >> 52;
     const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
-    const double kd = (double)k;
+    // (double)k without a conversion instruction: 2^52 + (k + 2^20) - (2^52 + 2^20), exact
+    const double kd = __dsub_rn(__hiloint2double(0x43300000, (int)(k + 0x100000)), 0x1p52 + 0x1p20);
     double invc, lc_hi, lc_lo;
     T.entry(i, invc, lc_hi, lc_lo);
     const LogConsts &K = T.C();

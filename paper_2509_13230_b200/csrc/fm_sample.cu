@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
     };
+    auto U01 = [](uint32_t k) { return kModel == FM_UBCM ? u01(k) : u01_cvt(k); };
     // u01 of the skip word, and the accept/weight words, of chain c's draw d[c] (R1, R2)
     auto draw_u = [&](const int c) {
         uint32_t ws;
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             wacc[c] = W.y;
             wwt[c] = W.z;
         }
-        return u01(ws);
+        return U01(ws);
     };
 
     for (;;) {
@@ -288,7 +289,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             if (act[c] && !fresh[c]) {
                 n_draw++;
                 const double R = __ddiv_rn(E[c], h[c]);
-                if (!(R < (double)(b[c] - 1 - cur[c]))) {  // terminal draw (R5)
+                // R < lim (lim = b-1-cur >= 0 an integer) <=> R < 2^31 and floor(R) < lim, with
+                // floor(R) the low word of RZ(R + 2^52) (exact for 0 <= R < 2^52): no I2F / F2I
+                const double Rt = __dadd_rz(R, 0x1p52);
+                const int32_t fl = __double2loint(Rt);
+                const bool step = R < 2147483648.0 && fl < b[c] - 1 - cur[c];
+                if (!step) {  // terminal draw (R5)
                     if (kStats && row_acc[c] && A.deg_row) {  // statistics mode: flush the row node's sums
                         atomicAdd(&A.deg_row[id_u[c]], (unsigned long long)row_acc[c]);
                         if (kModel == FM_ECM) atomicAdd(&A.str_row[id_u[c]], row_w[c]);
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     if (g[c] < g_end[c]) start_seg(c, true);
                     else act[c] = false;
                 } else {
-                    cur[c] = cur[c] + 1 + (int32_t)R;  // R >= 0: truncation == floor
+                    cur[c] = cur[c] + 1 + fl;  // floor(R)
                     // ECM: one 32-byte record per candidate (Plan::cand); id needed only if accepted
                     if (kModel == FM_ECM) {
                         const double2 v0 = __ldg(A.cand + 2 * (uint32_t)cur[c]);
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     const double D = __dadd_rn(1.0, X);
                     const double hn = fm_log1p(X, T);
                     if (landed[c]) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
-                        acc[c] = __dmul_rn(__dmul_rn(u01(w_land[c]), xq[c]), D) < __dmul_rn(X, dq[c]);
+                        acc[c] = __dmul_rn(__dmul_rn(U01(w_land[c]), xq[c]), D) < __dmul_rn(X, dq[c]);
                         xq[c] = X;
                         dq[c] = D;
                         h[c] = hn;
@@ -351,12 +357,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
                     const double hn = fm_log1p(__dmul_rn(z, iomT[c]), T);
                     if (landed[c]) {
-                        acc[c] = __dmul_rn(__dmul_rn(u01(w_land[c]), xq[c]), Dp) < __dmul_rn(z, dq[c]);
+                        acc[c] = __dmul_rn(__dmul_rn(U01(w_land[c]), xq[c]), Dp) < __dmul_rn(z, dq[c]);
                         xq[c] = z;
                         dq[c] = __dadd_rn(omT[c], z);
                         h[c] = hn;
                         if (acc[c]) {  // Eq. 5 weight, log t = log y_u + log y_v (R8)
-                            const double lu = fm_log(u01(w_wt[c]), T);
+                            const double lu = fm_log(U01(w_wt[c]), T);
                             const double G = floor(__ddiv_rn(lu, __dadd_rn(lyu[c], lyv[c])));
                             if (G <= 2147483646.0) {
                                 w[c] = 1 + (int32_t)G;
