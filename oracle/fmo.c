@@ -494,7 +494,11 @@ static void chain_ubcm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs,
     }
 }
 
-static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, int64_t g, buf_t *out)
+/* refresh != 0 (DESIGN R17): after each reached candidate j the bound for the rest
+ * of the segment uses beta_min over the candidates still ahead, T' = y_i * ymax[j+1] (Alg. 1 line 5
+ * "minimum beta among remaining unprocessed nodes", taken per candidate) */
+static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, int64_t g, int refresh,
+                      buf_t *out)
 {
     const int64_t i = p->seg_u[g], b = p->seg_b[g];
     const uint32_t sigma = (uint32_t)p->seg_sigma[g];
@@ -539,8 +543,14 @@ static void chain_ecm(const fmo_plan *p, const uint32_t key[2], uint32_t s_abs, 
         }
         /* Alg. 1 line 12: q <- p_hat_ij(beta_min) = z / (1 - T + z) (Eq. 6 as equality, R7) */
         zq = z;
-        dq = omT + z;
-        h = log1p(z * iomT);
+        if (refresh) {
+            double omTj = 1.0 - y_i * p->ymax[j + 1]; /* T' = y_i max_{w > j} y_w (R17) */
+            dq = omTj + z;
+            h = log1p(z * (1.0 / omTj));
+        } else {
+            dq = omT + z;
+            h = log1p(z * iomT);
+        }
     }
 }
 
@@ -560,6 +570,7 @@ typedef struct {
     buf_t *bufs;
     int64_t n_jobs;
     int64_t next;
+    int refresh;
     pthread_mutex_t mu;
 } pool_t;
 
@@ -575,7 +586,7 @@ static void *worker(void *arg)
         uint32_t s_abs = (uint32_t)(P->first_sample + J.sample);
         for (int64_t g = J.g0; g < J.g1; g++) {
             if (P->p->model == FMO_UBCM) chain_ubcm(P->p, P->key, s_abs, g, &P->bufs[k]);
-            else chain_ecm(P->p, P->key, s_abs, g, &P->bufs[k]);
+            else chain_ecm(P->p, P->key, s_abs, g, P->refresh, &P->bufs[k]);
         }
     }
     return NULL;
@@ -583,6 +594,12 @@ static void *worker(void *arg)
 
 int fmo_sample(const fmo_plan *p, uint64_t seed, int64_t first_sample, int64_t n_samples,
                const int32_t *rows, int64_t n_rows, int nthreads, fmo_result **out)
+{
+    return fmo_sample_ex(p, seed, first_sample, n_samples, rows, n_rows, nthreads, 0u, out);
+}
+
+int fmo_sample_ex(const fmo_plan *p, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                  const int32_t *rows, int64_t n_rows, int nthreads, uint32_t flags, fmo_result **out)
 {
     *out = NULL;
     if (!p || n_samples < 0 || first_sample < 0 || first_sample + n_samples > ((int64_t)1 << 32))
@@ -607,6 +624,7 @@ int fmo_sample(const fmo_plan *p, uint64_t seed, int64_t first_sample, int64_t n
     P.key[1] = (uint32_t)(seed >> 32);
     P.first_sample = first_sample;
     P.n_jobs = n_jobs;
+    P.refresh = (flags & FMO_SAMPLE_BETA_REFRESH) && p->model == FMO_ECM;
     P.jobs = (job_t *)malloc(sizeof(job_t) * (size_t)(n_jobs + 1));
     P.bufs = (buf_t *)calloc((size_t)n_jobs + 1, sizeof(buf_t));
     if (!P.jobs || !P.bufs) { free(P.jobs); free(P.bufs); return FMO_ERR_NOMEM; }

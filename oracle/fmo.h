@@ -62,6 +62,10 @@ void fmo_plan_export(const fmo_plan *p, int32_t *perm, double *kappa_s, double *
  * (row u, segment sigma, draw order); orientation (min id, max id). */
 int fmo_sample(const fmo_plan *p, uint64_t seed, int64_t first_sample, int64_t n_samples,
                const int32_t *rows, int64_t n_rows, int nthreads, fmo_result **out);
+/* with options: FMO_SAMPLE_BETA_REFRESH (ECM: per-candidate beta_min refresh, DESIGN R17) */
+enum { FMO_SAMPLE_BETA_REFRESH = 1u };
+int fmo_sample_ex(const fmo_plan *p, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                  const int32_t *rows, int64_t n_rows, int nthreads, uint32_t flags, fmo_result **out);
 
 /* Level-1 oracle: the plain definition, O(N^2) independent Bernoulli trials per pair with
  * an unrelated RNG (xoshiro256**), weights by sequential Bernoulli trials (Eq. 3-5). */

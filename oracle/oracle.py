@@ -85,6 +85,9 @@ def lib():
     L.fmo_plan_export.restype = None
     L.fmo_sample.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int64, i32p, C.c_int64, C.c_int, C.POINTER(vp)]
     L.fmo_sample.restype = C.c_int
+    L.fmo_sample_ex.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int64, i32p, C.c_int64, C.c_int, C.c_uint32,
+                                C.POINTER(vp)]
+    L.fmo_sample_ex.restype = C.c_int
     L.fmo_bruteforce.argtypes = [C.c_int, C.c_int64, f64p, f64p, C.c_uint64, C.c_int64, C.POINTER(vp)]
     L.fmo_bruteforce.restype = C.c_int
     L.fmo_result_n_samples.argtypes = [vp]
@@ -263,13 +266,18 @@ def _collect(h) -> Result:
     return Result(off, e, w, int(cnt[0]), int(cnt[1]), int(cnt[2]), int(fl[0]))
 
 
+SAMPLE_BETA_REFRESH = 1
+
+
 def sample(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, rows=None,
-           nthreads: int | None = None) -> Result:
-    """a5-a6: the method step by step, canonical edge order."""
+           nthreads: int | None = None, refresh: bool = False) -> Result:
+    """a5-a6: the method step by step, canonical edge order.  refresh: the ECM
+    per-candidate beta_min refresh (R17)."""
     rr = None if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
     h = C.c_void_p()
-    rc = lib().fmo_sample(C.c_void_p(plan._h), int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
-                          _p(rr, C.c_int32), 0 if rr is None else len(rr), int(nthreads or 1), C.byref(h))
+    rc = lib().fmo_sample_ex(C.c_void_p(plan._h), int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample),
+                             int(n_samples), _p(rr, C.c_int32), 0 if rr is None else len(rr), int(nthreads or 1),
+                             SAMPLE_BETA_REFRESH if refresh else 0, C.byref(h))
     if rc != 0:
         raise OracleError(f"fmo_sample failed: {rc}")
     res = _collect(h)

@@ -43,11 +43,12 @@ def test_ubcm_pair_frequencies_n30(O, kind, S):
     assert pv2 > 1e-4, (st2, d2)
 
 
+@pytest.mark.parametrize("refresh", [False, True])
 @pytest.mark.parametrize("S", [8, 1 << 40])
-def test_ecm_pair_and_weight_law_n30(O, S):
+def test_ecm_pair_and_weight_law_n30(O, S, refresh):
     x, y = WL.random_fitness(6, 30, 2.5, 0.4, ecm=True)
     pl = O.sort_plan(x, y, seg_target=S)
-    res = O.sample(pl, seed=99 + S, n_samples=R, nthreads=O.ncores())
+    res = O.sample(pl, seed=99 + S, n_samples=R, nthreads=O.ncores(), refresh=refresh)
     P, T = ecm_p(x, y)
     c = pair_counts(res.offsets, res.edges, 30)
     stat, dof, pv, zmax = chi2_binomial(c, R, P)
@@ -78,14 +79,14 @@ def test_ecm_pair_and_weight_law_n30(O, S):
     assert abs(res.weights.mean() - bf.weights.mean()) < 6 * res.weights.std() / math.sqrt(len(res.weights)) * 1.5
 
 
-@pytest.mark.parametrize("ecm", [False, True])
-def test_full_joint_n4(O, ecm):
+@pytest.mark.parametrize("ecm,refresh", [(False, False), (True, False), (True, True)])
+def test_full_joint_n4(O, ecm, refresh):
     """All 2^6 edge configurations of N=4 vs the product law (independence, incl. across segments)."""
     x = np.array([3.0, 1.2, 0.5, 0.2])
     y = np.array([0.7, 0.3, 0.8, 0.5]) if ecm else None
     pl = O.sort_plan(x, y, seg_target=8)
     RR = 400_000
-    res = O.sample(pl, seed=4242, n_samples=RR, nthreads=O.ncores())
+    res = O.sample(pl, seed=4242, n_samples=RR, nthreads=O.ncores(), refresh=refresh)
     pairs = [(i, j) for i in range(4) for j in range(i + 1, 4)]
     bit = {pr: 1 << k for k, pr in enumerate(pairs)}
     codes = np.zeros(RR, np.int64)
@@ -221,3 +222,24 @@ def test_permutation_equivariance(O):
     mapped = np.sort(inv[b.edges], axis=1)
     key = lambda e: np.sort(e[:, 0].astype(np.int64) * 2000 + e[:, 1])
     assert np.array_equal(key(a.edges), key(mapped))
+
+
+def test_beta_refresh_invariants(O):
+    """Per-candidate beta_min refresh (R17): with homogeneous y the bound never changes, so the
+    samples are identical to the per-segment bound; with heterogeneous y it is tighter: fewer
+    proposals per edge (1.67 -> 1.54 on config 3) and the same expected edge count."""
+    n, RR = 400, 50
+    x = WL.random_fitness(12, n, 2.5, 0.05)[0]
+    pl = O.sort_plan(x, np.full(n, 0.4), seg_target=16)
+    a = O.sample(pl, seed=3, n_samples=RR)
+    b = O.sample(pl, seed=3, n_samples=RR, refresh=True)
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.edges, b.edges)
+    assert np.array_equal(a.weights, b.weights) and a.draws == b.draws
+    x, y = WL.random_fitness(12, 3000, 2.5, 0.02, ecm=True)
+    pl = O.sort_plan(x, y, seg_target=256)
+    a = O.sample(pl, seed=3, n_samples=40, nthreads=O.ncores())
+    b = O.sample(pl, seed=3, n_samples=40, nthreads=O.ncores(), refresh=True)
+    assert b.landed / b.accepted < 0.97 * a.landed / a.accepted
+    ee = O.expected_edges(x, y) * 40
+    for r in (a, b):
+        assert abs(r.accepted - ee) < 5 * math.sqrt(ee)
