@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle work budget for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--refresh", action="store_true",
+                    help="ECM: per-candidate beta_min refresh (fm_sample_ecm_ex FM_SAMPLE_BETA_REFRESH, NEXT-4)")
     return ap.parse_args()
 
 
@@ -114,7 +116,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ roofline
-def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: int = 2):
+def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: int = 2, refresh: bool = False):
     """Roofline of the dominant kernel k_sample.
 
     Compute term: algorithmic warp-instructions of the chain (op list of DESIGN 7.1, per-op
@@ -132,7 +134,10 @@ def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: i
     sms = C["sm_count"]
     issue_peak = C["issue_warp_inst_per_clk_per_sm"] * sms * clk            # warp-inst/s
     fp64_peak = C["fp64_warp_inst_per_clk_per_sm"] * sms * clk               # warp-inst/s
-    per = C["per_unit"][model]
+    per = {k: dict(v) for k, v in C["per_unit"][model].items()}
+    if refresh:  # per landed: + Ymax[cur+1] gather (2), y_u * Ymax, 1 - T', RN(1/(1-T')) (a division)
+        d = C["per_op_warp_inst"]["ddiv"]
+        per["landed"] = {"inst": per["landed"]["inst"] + 4 + d["inst"], "fp64": per["landed"]["fp64"] + 2 + d["fp64"]}
     draws, landed, acc = counters["draws"], counters["landed"], counters["accepted"]
     units = {"draw": draws, "landed": landed, "accepted": acc}
     inst = sum(units[u] * per[u]["inst"] for u in units) / 32.0             # warp-instructions
@@ -151,7 +156,7 @@ def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: i
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        tr = json.load(open(tpath)).get("k_sample", {}).get(f"{model}_cfg{cfg}")
+        tr = json.load(open(tpath)).get("k_sample", {}).get(f"{model}_cfg{cfg}" + ("_refresh" if refresh else ""))
         if tr:
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
     return {"bound": "alu" if bound != "hbm" else "hbm", "resource": bound, "achieved": ach, "peak": peak,
@@ -166,7 +171,7 @@ def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: i
 
 
 # ------------------------------------------------------------------------------------------ oracle
-def cpu_oracle_run(w, x, y, seg_target, budget_s):
+def cpu_oracle_run(w, x, y, seg_target, budget_s, refresh=False):
     """Time the oracle as it stands on the host cores on a bounded sample of the workload."""
     from oracle import oracle as O
     O.build()
@@ -176,11 +181,11 @@ def cpu_oracle_run(w, x, y, seg_target, budget_s):
     t_plan = time.perf_counter() - t0
     # probe with one sample, then size the run to ~budget_s
     t0 = time.perf_counter()
-    O.sample(plan, w.seed, n_samples=1, first_sample=0, nthreads=nth)
+    O.sample(plan, w.seed, n_samples=1, first_sample=0, nthreads=nth, refresh=refresh)
     t1 = time.perf_counter() - t0
     R = int(max(1, min(w.n_samples, budget_s / max(t1, 1e-6))))
     t0 = time.perf_counter()
-    r = O.sample(plan, w.seed, n_samples=R, first_sample=0, nthreads=nth)
+    r = O.sample(plan, w.seed, n_samples=R, first_sample=0, nthreads=nth, refresh=refresh)
     dt = time.perf_counter() - t0
     # per-sample plan cost amortised like the GPU step: plan once per R samples of a step
     step_s = dt + t_plan * (R / w.n_samples)
@@ -188,6 +193,19 @@ def cpu_oracle_run(w, x, y, seg_target, budget_s):
             "sample": f"{R} of the {w.n_samples} samples of {w.name} (+ plan time pro-rated), seed {w.seed}",
             "proposals_per_s": r.landed / step_s, "draws_per_s": r.draws / step_s, "seconds": dt + t_plan,
             "edges": r.accepted}
+
+
+METRIC = "accepted edges/s (proposals/s alongside); % of sampler roofline"
+
+
+def config_dict(w, args, R, world):
+    """The workload of a bench line (both arms)."""
+    return {"workload": w.name, "model": w.model, "n": w.n, "gamma": w.gamma, "kbar": w.kbar,
+            "samples_per_step_per_gpu": R, "seg_target": args.seg_target, "seed": w.seed,
+            "step": "fm_sort_plan + fm_sample_%s(%d samples) + free" % (w.model, R),
+            "beta_refresh": bool(args.refresh and w.model == "ecm"),
+            "l2": "256 MiB write between timed steps (outside events); output per step > L2",
+            "parallelism": f"sample-parallel x{world} (no data-path collective)"}
 
 
 def run_reference(args):
@@ -198,16 +216,16 @@ def run_reference(args):
     x, y = WL.fitness(w)
     res = []
     for i in range(args.warmup + args.steps):
-        c = cpu_oracle_run(w, x, y, args.seg_target, max(1.0, args.cpu_seconds / max(1, args.steps)))
+        c = cpu_oracle_run(w, x, y, args.seg_target, max(1.0, args.cpu_seconds / max(1, args.steps)),
+                           refresh=args.refresh)
         if i >= args.warmup:
             res.append(c)
     v = statistics.median([c["value"] for c in res])
-    line = {"impl": "reference", "metric": "accepted edges/s (proposals/s alongside)", "value": v, "unit": "edges/s",
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.median([c["seconds"] for c in res]), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w.name, "model": w.model, "n": w.n, "samples_per_step": w.n_samples,
-                       "seg_target": args.seg_target},
+            "config": config_dict(w, args, w.n_samples, 1),
             "cpu_baseline": {k: res[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": v},
             "proposals_per_s": statistics.median([c["proposals_per_s"] for c in res]),
             "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -234,7 +252,11 @@ def run_own(args):
     yd = None if y is None else torch.from_numpy(y).cuda()
     R = w.n_samples
     first, _ = D.shard_samples(rank, world, R)
-    sample = fm.sample_ubcm if w.model == "ubcm" else fm.sample_ecm
+    if w.model == "ubcm":
+        sample = fm.sample_ubcm
+    else:
+        def sample(plan, seed, **kw):
+            return fm.sample_ecm(plan, seed, refresh=args.refresh, **kw)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step():
@@ -320,22 +342,19 @@ def run_own(args):
             dist.destroy_process_group()
         return
 
-    rf = roofline(w.model, tot, tim["sample_ms"], max(1, tim["sample_launches"]), cfg=args.config)
+    refresh = args.refresh and w.model == "ecm"
+    rf = roofline(w.model, tot, tim["sample_ms"], max(1, tim["sample_launches"]), cfg=args.config, refresh=refresh)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        c = cpu_oracle_run(w, x, y, args.seg_target, args.cpu_seconds)
+        c = cpu_oracle_run(w, x, y, args.seg_target, args.cpu_seconds, refresh=refresh)
         cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
         cpu["proposals_per_s"] = c["proposals_per_s"]
     line = {
-        "metric": "accepted edges/s (proposals/s alongside); % of sampler roofline",
+        "metric": METRIC,
         "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "model": w.model, "n": w.n, "gamma": w.gamma, "kbar": w.kbar,
-                   "samples_per_step_per_gpu": R, "seg_target": args.seg_target, "seed": w.seed,
-                   "step": "fm_sort_plan + fm_sample_%s(%d samples) + free" % (w.model, R),
-                   "l2": "256 MiB write between timed steps (outside events); output per step > L2",
-                   "parallelism": f"sample-parallel x{world} (no data-path collective)"},
+        "config": config_dict(w, args, R, world),
         "proposals_per_s": landed_all / (t_max * 1e-3), "draws_per_s": draws_all / (t_max * 1e-3),
         "edges_per_step": edges_all / args.steps / world,
         "phase_ms_per_step": {"plan": tim["plan_ms"] / args.steps, "sample_kernel": tim["sample_ms"] / args.steps,

@@ -120,6 +120,17 @@ fm_status fm_sample_ubcm(const fm_plan *plan, uint64_t seed, int64_t first_sampl
 fm_status fm_sample_ecm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
                         void *cuda_stream, fm_edges *out);
 
+/* Sampling options (fm_sample_ecm_ex). */
+enum { FM_SAMPLE_BETA_REFRESH = 1u };
+/* As fm_sample_ecm with options.  FM_SAMPLE_BETA_REFRESH (R17): after each
+ * reached candidate cur the bound for the candidates still ahead uses beta_min over them,
+ * T' = y_u * max_{w > cur} y_w (Alg. 1 line 5 "minimum beta among remaining unprocessed nodes",
+ * P:L153, taken per candidate) instead of the segment-start value: fewer proposals per edge
+ * (about 7 % on config 3), the same law, different random streams' use, so a different (equally
+ * valid) sample than without the flag.  Unknown flags: FM_ERR_INVALID. */
+fm_status fm_sample_ecm_ex(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                           uint32_t flags, void *cuda_stream, fm_edges *out);
+
 /* Counters of a statistics-mode call (sums over its samples). */
 typedef struct {
     int64_t draws, landed, accepted;

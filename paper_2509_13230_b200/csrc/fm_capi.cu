@@ -503,7 +503,7 @@ static TaskMap make_task_map(const Plan *p, int64_t n_samples, int64_t *n_tasks)
 }
 
 static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
-                             void *cuda_stream, fm_edges *out)
+                             uint32_t flags, void *cuda_stream, fm_edges *out)
 {
     if (!out) return fail(FM_ERR_INVALID, "out is NULL");
     memset(out, 0, sizeof(*out));
@@ -578,6 +578,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.ly_s = p->cly;
         a.perm = p->cperm;
         a.cand = p->cand;
+        a.ymax_c = (model == FM_ECM && (flags & FM_SAMPLE_BETA_REFRESH)) ? p->ymax : nullptr;
         a.ordered = p->kind != FM_UNDIRECTED;
         a.tm = tm;
         a.key = philox_key(seed);
@@ -793,13 +794,23 @@ static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, 
 fm_status fm_sample_ubcm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
                          void *cuda_stream, fm_edges *out)
 {
-    return sample_impl(FM_UBCM, plan, seed, first_sample, n_samples, cuda_stream, out);
+    return sample_impl(FM_UBCM, plan, seed, first_sample, n_samples, 0u, cuda_stream, out);
 }
 
 fm_status fm_sample_ecm(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
                         void *cuda_stream, fm_edges *out)
 {
-    return sample_impl(FM_ECM, plan, seed, first_sample, n_samples, cuda_stream, out);
+    return sample_impl(FM_ECM, plan, seed, first_sample, n_samples, 0u, cuda_stream, out);
+}
+
+fm_status fm_sample_ecm_ex(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
+                           uint32_t flags, void *cuda_stream, fm_edges *out)
+{
+    if (flags & ~(uint32_t)FM_SAMPLE_BETA_REFRESH) {
+        if (out) memset(out, 0, sizeof(*out));
+        return fail(FM_ERR_INVALID, "unknown fm_sample_ecm_ex flags 0x%x", flags);
+    }
+    return sample_impl(FM_ECM, plan, seed, first_sample, n_samples, flags, cuda_stream, out);
 }
 
 fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host, void *cuda_stream)

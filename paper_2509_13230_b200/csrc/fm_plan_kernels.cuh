@@ -103,6 +103,7 @@ struct SampleArgs {
     const double *kappa_s, *y_s, *ly_s;  // CANDIDATE arrays (the - set; the rows themselves if undirected)
     const int32_t *perm;                 // candidate rank -> id
     const double2 *cand;                 // packed gather records (Plan::cand)
+    const double *ymax_c;                // ECM beta_min refresh (R17): candidate Ymax [nc+1]; NULL = per segment
     TaskMap tm;                    // task -> (sample, chunking, lane-chunk) and scratch slots
     PhiloxKey key;
     LogConsts lc;                  // log polynomial constants (read as parameter-bank operands)

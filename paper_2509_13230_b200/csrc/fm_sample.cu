@@ -71,7 +71,7 @@ __device__ __forceinline__ uint32_t load_logtab()
 // parallelism (instantiated with kC = 1: two chains measured slower, their registers cost more
 // occupancy than their ILP gains).
 // kStats: statistics mode (fm_sample_degrees): degree / strength sums instead of edge lists.
-template <int kModel, int kMinBlocks, int kC, bool kStats>
+template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         // ---- 3. consume one draw per chain ----
         bool landed[kC];
         uint32_t w_land[kC], w_wt[kC];
-        double kv[kC], yv[kC], lyv[kC];
+        double kv[kC], yv[kC], lyv[kC], ymn[kC];
         int32_t id_v[kC];
 #pragma unroll
         for (int c = 0; c < kC; c++) {
@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             if (kModel == FM_ECM) {
                 kv[c] = yv[c] = lyv[c] = 0.0;
                 id_v[c] = 0;
+                ymn[c] = 0.0;
             }
             if (act[c] && !fresh[c]) {
                 n_draw++;
@@ -313,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         yv[c] = v0.y;
                         lyv[c] = v1.x;
                         id_v[c] = __double2loint(v1.y);
+                        if (kRefresh) ymn[c] = __ldg(A.ymax_c + cur[c] + 1);
                     } else {  // (UBCM: two plain gathers measured faster than the 16-byte record)
                         kv[c] = A.kappa_s[cur[c]];
                         id_v[c] = A.perm[cur[c]];
@@ -355,11 +357,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(us, 0.0))) : 1.0;
                     const double t = __dmul_rn(yu[c], yv[c]);  // (ECM: yv defined on every path, see above)
                     const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
-                    const double hn = fm_log1p(__dmul_rn(z, iomT[c]), T);
+                    // the bound for the candidates still ahead: per segment 1 - T = omT, or (kRefresh,
+                    // R17) per reached candidate 1 - y_u Ymax[cur+1]
+                    double omb = omT[c], iomb = iomT[c];
+                    if (kRefresh && landed[c]) {
+                        omb = __dsub_rn(1.0, __dmul_rn(yu[c], ymn[c]));
+                        iomb = __drcp_rn(omb);
+                    }
+                    const double hn = fm_log1p(__dmul_rn(z, iomb), T);
                     if (landed[c]) {
                         acc[c] = __dmul_rn(__dmul_rn(U01(w_land[c]), xq[c]), Dp) < __dmul_rn(z, dq[c]);
                         xq[c] = z;
-                        dq[c] = __dadd_rn(omT[c], z);
+                        dq[c] = __dadd_rn(omb, z);
                         h[c] = hn;
                         if (acc[c]) {  // Eq. 5 weight, log t = log y_u + log y_v (R8)
                             const double lu = fm_log(U01(w_wt[c]), T);
@@ -591,9 +600,8 @@ cudaError_t ensure_log_table(cudaStream_t st)
     return e;
 }
 
-// the sampler is instantiated for several register budgets (min resident blocks per SM);
-// FM_SAMPLE_MINB selects one at run time (tuning), default per model
-template <int kModel, int kMinB, int kC, bool kStats>
+// one instantiation per (model, statistics mode, ECM bound refresh); kMinB = 3 blocks per SM
+template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
     int dev = 0, sms = 0, per = 0;
@@ -602,7 +610,7 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
     const size_t dyn = (size_t)kThreads * kC * (kModel == FM_ECM ? 96 : 64);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats, kRefresh>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)dyn);
         // shared-memory carveout (percent of the unified L1/shared capacity): the driver's default
         // picked 135 KB of shared memory for 3 x 27 KB of need; 40 % leaves more L1 for the kappa /
@@ -610,29 +618,17 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         // overrides (-1 = driver default)
         const char *cv = getenv("FM_SAMPLE_CARVEOUT");
         const int carve = cv && *cv ? atoi(cv) : 40;
-        if (carve >= 0) cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats>,
+        if (carve >= 0) cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats, kRefresh>,
                                              cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         attr_set = true;
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC, kStats>, kThreads, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC, kStats, kRefresh>, kThreads, dyn);
     int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
     const int64_t need = (a.n_tasks + kThreads * kC - 1) / (kThreads * kC);  // <= one task per chain at start
     if (need < blocks) blocks = need;
     count_launch();
-    k_sample<kModel, kMinB, kC, kStats><<<(unsigned)blocks, kThreads, dyn, st>>>(a);
+    k_sample<kModel, kMinB, kC, kStats, kRefresh><<<(unsigned)blocks, kThreads, dyn, st>>>(a);
     return cudaGetLastError();
-}
-
-// one chain per thread (kC = 2 measured slower: register-limited occupancy); FM_SAMPLE_MINB
-// overrides the blocks-per-SM target of the register budget (tuning experiments)
-template <int kModel, bool kStats>
-static cudaError_t launch_sample_m(int minb, const SampleArgs &a, cudaStream_t st)
-{
-    switch (minb) {
-    case 2: return launch_sample_t<kModel, 2, 1, kStats>(a, st);
-    case 4: return launch_sample_t<kModel, 4, 1, kStats>(a, st);
-    default: return launch_sample_t<kModel, 3, 1, kStats>(a, st);
-    }
 }
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
@@ -646,12 +642,14 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
         e = cudaMemsetAsync(a.spill_counter, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
     }
-    const char *ev = getenv("FM_SAMPLE_MINB");
-    const int minb = ev && *ev ? atoi(ev) : 3;  // 24 warps/SM (measured best for both models)
+    // one chain per thread, 3 blocks of 256 per SM (kC = 2, 2 or 4 blocks per SM measured slower)
     const bool stats = a.deg_row != nullptr || a.rank_hist != nullptr;
     if (model == FM_UBCM)
-        return stats ? launch_sample_m<FM_UBCM, true>(minb, a, st) : launch_sample_m<FM_UBCM, false>(minb, a, st);
-    return stats ? launch_sample_m<FM_ECM, true>(minb, a, st) : launch_sample_m<FM_ECM, false>(minb, a, st);
+        return stats ? launch_sample_t<FM_UBCM, 3, 1, true, false>(a, st)
+                     : launch_sample_t<FM_UBCM, 3, 1, false, false>(a, st);
+    if (stats) return launch_sample_t<FM_ECM, 3, 1, true, false>(a, st);
+    return a.ymax_c ? launch_sample_t<FM_ECM, 3, 1, false, true>(a, st)
+                    : launch_sample_t<FM_ECM, 3, 1, false, false>(a, st);
 }
 
 cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *spill_off,

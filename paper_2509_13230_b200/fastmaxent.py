@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ER
                 -5: "FM_ERR_STATE"}
 FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
 _KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
-SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_edges_to_host", "fm_plan_get_info",
+SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_sample_ecm_ex", "fm_edges_to_host", "fm_plan_get_info",
            "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval"]
 
 
@@ -75,6 +75,8 @@ def _load():
     for f in (L.fm_sample_ubcm, L.fm_sample_ecm):
         f.argtypes = [vp, u64, i64, i64, vp, C.POINTER(_Edges)]
         f.restype = C.c_int
+    L.fm_sample_ecm_ex.argtypes = [vp, u64, i64, i64, C.c_uint32, vp, C.POINTER(_Edges)]
+    L.fm_sample_ecm_ex.restype = C.c_int
     L.fm_sample_degrees.argtypes = [vp, u64, i64, i64, vp, vp, vp, vp, vp, C.POINTER(_Counters)]
     L.fm_sample_degrees.restype = C.c_int
     L.fm_sample_richclub.argtypes = [vp, u64, i64, i64, vp, vp, C.POINTER(_Counters)]
@@ -311,9 +313,20 @@ def sample_ubcm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0
     return _sample(lib.fm_sample_ubcm, plan, seed, n_samples, first_sample, stream)
 
 
-def sample_ecm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None) -> Edges:
-    """fm_sample_ecm (Algorithm 1)."""
-    return _sample(lib.fm_sample_ecm, plan, seed, n_samples, first_sample, stream)
+FM_SAMPLE_BETA_REFRESH = 1
+
+
+def sample_ecm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None,
+               refresh: bool = False) -> Edges:
+    """fm_sample_ecm (Algorithm 1); refresh=True: fm_sample_ecm_ex with
+    FM_SAMPLE_BETA_REFRESH (per-candidate beta_min, R17)."""
+    if not refresh:
+        return _sample(lib.fm_sample_ecm, plan, seed, n_samples, first_sample, stream)
+    st = _Edges()
+    s = _stream(stream)
+    _check(lib.fm_sample_ecm_ex(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
+                                FM_SAMPLE_BETA_REFRESH, s, C.byref(st)))
+    return Edges(st, s)
 
 
 def sample_degrees(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0, stream=None):
