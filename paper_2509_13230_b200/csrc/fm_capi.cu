@@ -161,12 +161,6 @@ void plan_release(Plan *p)
     cudaFree(p->kappa_s);
     cudaFree(p->y_s);
     cudaFree(p->ymax);
-    cudaFree(p->sa.seg);
-    cudaFree(p->sa.h0);
-    cudaFree(p->sa.x0);
-    cudaFree(p->sa.d0);
-    cudaFree(p->sa.omT);
-    cudaFree(p->sa.iomT);
     cudaFree(p->ly_s);
     cudaFree(p->rec);
     for (int k = 0; k < 2; k++) {
@@ -230,7 +224,8 @@ static fm_status sort_node_set(int model, int64_t n, const double *x, const doub
     CK(tmp.get(&ia, n), "alloc ids");
     CK(tmp.get(&ib, n), "alloc ids");
     count_launch();
-    k_validate_key<<<grid_for(n, 256), 256, 0, st>>>(model, n, xd, yd, ka, ia, sc, hist);
+    k_validate_key<<<(unsigned)std::min<int64_t>(grid_for(n, 256), 148 * 8), 256, 0, st>>>(model, n, xd, yd, ka, ia,
+                                                                                             sc, hist);
     CK(cudaGetLastError(), "k_validate_key");
     const size_t tb = radix_tmp_bytes(n);
     char *work;
@@ -389,23 +384,16 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     p->wmax = h_sc.wmax;
     p->est_draws = h_sc.total_work >> kG;
     // row_m now holds row_seg (exclusive prefix of the per-row segment counts, n+1 entries)
-    {
-        const size_t ns = (size_t)std::max<int64_t>(n_seg, 1);
-        CK(cudaMallocAsync((void **)&p->sa.seg, sizeof(int4) * ns, st), "alloc seg");
-        double **arrs[5] = {&p->sa.h0, &p->sa.x0, &p->sa.d0, &p->sa.omT, &p->sa.iomT};
-        for (double **a : arrs) CK(cudaMallocAsync((void **)a, sizeof(double) * ns, st), "alloc seg arrays");
-    }
     int64_t *seg_work;
     CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
-    count_launch();
-    k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, (int)kind, n1, nc, n_seg, p->kappa_s, p->y_s, p->ckappa,
-                                                 p->ymax, P, sc, rows, row_m, p->sa, seg_work);
-    CK(cudaGetLastError(), "k_emit");
     CK(cudaMallocAsync((void **)&p->rec, sizeof(SegRec) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
-    count_launch();
-    k_pack<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, n_seg, p->sa, p->kappa_s, p->perm, p->y_s, p->ly_s,
-                                                 p->excl, p->rec);
-    CK(cudaGetLastError(), "k_pack");
+    if (n_seg > 0) {
+        count_launch();
+        k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, (int)kind, n1, nc, n_seg, p->kappa_s, p->y_s,
+                                                     p->ly_s, p->perm, p->excl, p->ckappa, p->ymax, P, sc, rows,
+                                                     row_m, p->rec, seg_work);
+        CK(cudaGetLastError(), "k_emit");
+    }
     {
         const size_t wb = scan_tmp_bytes(n_seg + 1);
         char *work2;
@@ -863,12 +851,23 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (y_s && p->y_s) CK(cudaMemcpy(y_s, p->y_s, n * 8, cudaMemcpyDeviceToHost), "y_s");
     if (ymax && p->ymax) CK(cudaMemcpy(ymax, p->ymax, ((size_t)p->nc + 1) * 8, cudaMemcpyDeviceToHost), "ymax");
     if (ly_s && p->ly_s) CK(cudaMemcpy(ly_s, p->ly_s, n * 8, cudaMemcpyDeviceToHost), "ly_s");
-    if (seg && s) CK(cudaMemcpy(seg, p->sa.seg, s * 16, cudaMemcpyDeviceToHost), "seg");
-    if (seg_h0 && s) CK(cudaMemcpy(seg_h0, p->sa.h0, s * 8, cudaMemcpyDeviceToHost), "seg_h0");
-    if (seg_x0 && s) CK(cudaMemcpy(seg_x0, p->sa.x0, s * 8, cudaMemcpyDeviceToHost), "seg_x0");
-    if (seg_d0 && s) CK(cudaMemcpy(seg_d0, p->sa.d0, s * 8, cudaMemcpyDeviceToHost), "seg_d0");
-    if (seg_omT && s) CK(cudaMemcpy(seg_omT, p->sa.omT, s * 8, cudaMemcpyDeviceToHost), "seg_omT");
-    if (seg_iomT && s) CK(cudaMemcpy(seg_iomT, p->sa.iomT, s * 8, cudaMemcpyDeviceToHost), "seg_iomT");
+    if (s && (seg || seg_h0 || seg_x0 || seg_d0 || seg_omT || seg_iomT)) {  // from the packed records
+        std::vector<SegRec> r(s);
+        CK(cudaMemcpy(r.data(), p->rec, s * sizeof(SegRec), cudaMemcpyDeviceToHost), "seg records");
+        for (size_t g = 0; g < s; g++) {
+            if (seg) {
+                seg[4 * g] = r[g].u;
+                seg[4 * g + 1] = r[g].a;
+                seg[4 * g + 2] = r[g].b;
+                seg[4 * g + 3] = r[g].sigma;
+            }
+            if (seg_h0) seg_h0[g] = r[g].h0;
+            if (seg_x0) seg_x0[g] = r[g].x0;
+            if (seg_d0) seg_d0[g] = r[g].d0;
+            if (seg_omT) seg_omT[g] = r[g].omT;
+            if (seg_iomT) seg_iomT[g] = r[g].iomT;
+        }
+    }
     return FM_OK;
 }
 

@@ -31,12 +31,6 @@ struct __align__(16) SegRec {
     double omT, iomT;        // ECM: 1 - T, RN(1 / (1 - T))
 };
 
-// per-segment plan arrays (SoA, exported for tests; k_pack builds SegRec from them)
-struct SegArrays {
-    int4 *seg;  // (u, a, b, sigma)
-    double *h0, *x0, *d0, *omT, *iomT;
-};
-
 // double2 words per candidate in Plan::cand (one 16- or 32-byte record: one L2 sector per gather)
 __host__ __device__ constexpr int kCandWords(int model) { return model == 0 ? 1 : 2; }
 
@@ -60,7 +54,6 @@ struct Plan {
                         //   (kappa, y), (log y, id); id in the low word.  NULL for UBCM
     // a4 segments
     int64_t n_seg;
-    SegArrays sa;       // [n_seg] each
     double *ly_s;       // [n] ECM: log y_s
     SegRec *rec;        // [n_seg] packed copy of the above for the sampler
     int64_t est_draws;  // sum of segment work estimates / 2^G

@@ -18,14 +18,22 @@ __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, cons
                                                       int32_t *__restrict__ ids, PlanScalars *sc,
                                                       unsigned int *__restrict__ hist)
 {
-    // also: the radix digit histograms of all 8 byte positions (fm_sort.cu consumes them)
+    // also: the radix digit histograms of all 8 byte positions (fm_sort.cu consumes them).
+    // Grid-stride (a bounded grid): each block accumulates in shared memory and flushes its
+    // 8 x 256 counts and its key OR/AND once.
     __shared__ unsigned int h[8][256];
+    __shared__ unsigned long long s_or, s_and;
+    __shared__ int s_bad;
     for (int p = 0; p < 8; p++) h[p][threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        s_or = 0;
+        s_and = ~0ull;
+        s_bad = 0;
+    }
     __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t kor = 0, kand = ~0ull;
     bool bad = false;
-    if (i < n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double xi = x[i];
         bool ok = isfinite(xi) && xi >= 0.0;
         double kappa = xi;
@@ -40,15 +48,12 @@ __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, cons
         const uint64_t key = ~(uint64_t)__double_as_longlong(kappa);
         keys[i] = key;
         ids[i] = (int32_t)i;
-        kor = key;
-        kand = key;
-        bad = !ok;
+        kor |= key;
+        kand &= key;
+        bad = bad || !ok;
 #pragma unroll
         for (int p = 0; p < 8; p++) atomicAdd(&h[p][(key >> (8 * p)) & 0xFF], 1u);
     }
-    __syncthreads();
-    for (int p = 0; p < 8; p++)
-        if (h[p][threadIdx.x]) atomicAdd(&hist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kor |= __shfl_xor_sync(0xffffffffu, kor, o);
@@ -56,9 +61,17 @@ __global__ void __launch_bounds__(256) k_validate_key(int model, int64_t n, cons
     }
     const bool anybad = __any_sync(0xffffffffu, bad);
     if ((threadIdx.x & 31) == 0) {
-        atomicOr(&sc->key_or, (unsigned long long)kor);
-        atomicAnd(&sc->key_and, (unsigned long long)kand);
-        if (anybad) atomicOr(&sc->flags, kErrInvalid);
+        atomicOr(&s_or, (unsigned long long)kor);
+        atomicAnd(&s_and, (unsigned long long)kand);
+        if (anybad) s_bad = 1;
+    }
+    __syncthreads();
+    for (int p = 0; p < 8; p++)
+        if (h[p][threadIdx.x]) atomicAdd(&hist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
+    if (threadIdx.x == 0) {
+        atomicOr(&sc->key_or, s_or);
+        atomicAnd(&sc->key_and, s_and);
+        if (s_bad) atomicOr(&sc->flags, kErrInvalid);
     }
 }
 
@@ -143,15 +156,29 @@ __global__ void __launch_bounds__(256) k_rows(int model, int kind, int64_t n, in
             row_m[u] = 0;  // no candidates (the last undirected row): no segment, no draw
         }
     }
-    // block reduce of work (int64)
+    // block reduce of work (int64): one pair of global atomics per block (a per-warp pair made
+    // the 1e7-row plan wait ~0.5 ms on two contended addresses)
+    __shared__ long long s_work[8], s_wseg[8];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         work += __shfl_xor_sync(0xffffffffu, work, o);
         wseg = max(wseg, __shfl_xor_sync(0xffffffffu, wseg, o));
     }
-    if ((threadIdx.x & 31) == 0 && work) {
-        atomicAdd((unsigned long long *)&sc->total_work, (unsigned long long)work);
-        atomicMax(&sc->wmax, wseg);
+    if ((threadIdx.x & 31) == 0) {
+        s_work[threadIdx.x >> 5] = work;
+        s_wseg[threadIdx.x >> 5] = wseg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long tw = 0, tm = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            tw += s_work[w];
+            tm = max(tm, s_wseg[w]);
+        }
+        if (tw) {
+            atomicAdd((unsigned long long *)&sc->total_work, (unsigned long long)tw);
+            atomicMax(&sc->wmax, tm);
+        }
     }
 }
 
@@ -169,22 +196,37 @@ __device__ __forceinline__ int64_t plan_cut(const uint64_t *P, int F, int64_t nc
     return lo;
 }
 
-// a4 step 5-6 (per segment): (u, a, b, sigma), initial bound (x0, d0, h0, omT), work estimate
+// a4 step 5-6 (per segment): (u, a, b, sigma), initial bound (x0, d0, h0, omT), work estimate,
+// written straight into the sampler's packed record (SegRec)
 __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg,
                                               const double *__restrict__ kappa_s, const double *__restrict__ y_s,
-                                              const double *__restrict__ ckappa, const double *__restrict__ ymax,
-                                              const uint64_t *__restrict__ P, PlanScalars *sc,
-                                              const RowInfo *__restrict__ rows, const int64_t *__restrict__ row_seg,
-                                              SegArrays sa, int64_t *__restrict__ seg_work)
+                                              const double *__restrict__ ly_s, const int32_t *__restrict__ perm,
+                                              const int32_t *__restrict__ excl, const double *__restrict__ ckappa,
+                                              const double *__restrict__ ymax, const uint64_t *__restrict__ P,
+                                              PlanScalars *sc, const RowInfo *__restrict__ rows,
+                                              const int64_t *__restrict__ row_seg, SegRec *__restrict__ rec,
+                                              int64_t *__restrict__ seg_work)
 {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n_seg) return;
-    const int F = sc->F;
-    // row u: largest u with row_seg[u] <= g; every row that has candidates has >= 1 segment, so
-    // u lies in [g - extra, g] (rows with candidates: n-1 undirected, all n otherwise)
+    __shared__ int64_t s_u0;
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t g = g0 + threadIdx.x;
+    // row u of segment g: largest u with row_seg[u] <= g.  Every row that has candidates has >= 1
+    // segment (rows with candidates: n-1 undirected, all n otherwise), so u(g) lies in
+    // [g - extra, g]; the block's first row u0 is found once, then u(g) in [u0, u0 + (g - g0)]
     const int64_t rows_w = kind == FM_UNDIRECTED ? n - 1 : n;
     const int64_t extra = n_seg - rows_w;
-    int64_t lo = g - extra > 0 ? g - extra : 0, hi = g < rows_w - 1 ? g : rows_w - 1;
+    if (threadIdx.x == 0) {
+        int64_t lo = g0 - extra > 0 ? g0 - extra : 0, hi = g0 < rows_w - 1 ? g0 : rows_w - 1;
+        while (lo < hi) {
+            const int64_t mid = lo + ((hi - lo + 1) >> 1);
+            if (row_seg[mid] <= g0) lo = mid; else hi = mid - 1;
+        }
+        s_u0 = lo;
+    }
+    __syncthreads();
+    if (g >= n_seg) return;
+    const int F = sc->F;
+    int64_t lo = s_u0, hi = s_u0 + (g - g0) < rows_w - 1 ? s_u0 + (g - g0) : rows_w - 1;
     while (lo < hi) {
         const int64_t mid = lo + ((hi - lo + 1) >> 1);
         if (row_seg[mid] <= g) lo = mid; else hi = mid - 1;
@@ -198,25 +240,39 @@ __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, in
     a = sigma == 0 ? c0 : plan_cut(P, F, nc, c0, ri, m, sigma);
     b = sigma == m - 1 ? nc : plan_cut(P, F, nc, c0, ri, m, sigma + 1);
     if (!(a < b) || !(a >= c0)) atomicOr(&sc->flags, kErrState);
-    sa.seg[g] = make_int4((int)u, (int)a, (int)b, (int)sigma);
+    SegRec r;
+    r.u = (int)u;
+    r.a = (int)a;
+    r.b = (int)b;
+    r.sigma = (int)sigma;
     // bound at the virtual previous position a-1 (R3); a bipartite row start uses candidate 0 (R16)
     const int64_t bp = a > 0 ? a - 1 : 0;
-    const double kq = __dmul_rn(kappa_s[u], ckappa[bp]);
-    sa.x0[g] = kq;
+    const double ku = kappa_s[u];
+    const double kq = __dmul_rn(ku, ckappa[bp]);
+    r.x0 = kq;
+    r.ku = ku;
+    r.id_u = perm[u];
+    r.excl = excl ? excl[u] : -1;
+    r.pad1 = r.pad2 = 0;
     if (model == FM_UBCM) {
-        sa.omT[g] = 1.0;
-        sa.iomT[g] = 1.0;
-        sa.d0[g] = __dadd_rn(1.0, kq);
-        sa.h0[g] = log1p(kq);
+        r.omT = 1.0;
+        r.iomT = 1.0;
+        r.d0 = __dadd_rn(1.0, kq);
+        r.h0 = log1p(kq);
+        r.yu = 0.0;
+        r.ly_u = 0.0;
     } else {
         const double T = __dmul_rn(y_s[u], ymax[a]);
         const double omT = __dsub_rn(1.0, T);
         const double iomT = __ddiv_rn(1.0, omT);
-        sa.omT[g] = omT;
-        sa.iomT[g] = iomT;
-        sa.d0[g] = __dadd_rn(omT, kq);
-        sa.h0[g] = log1p(__dmul_rn(kq, iomT));
+        r.omT = omT;
+        r.iomT = iomT;
+        r.d0 = __dadd_rn(omT, kq);
+        r.h0 = log1p(__dmul_rn(kq, iomT));
+        r.yu = y_s[u];
+        r.ly_u = ly_s[u];
     }
+    rec[g] = r;
     const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, c0, ri.r, ri.sat, a);
     const int64_t wb = plan_W(P, F, c0, ri.r, ri.sat, b);
     seg_work[g] = wb - wa + kUnit;
@@ -258,34 +314,6 @@ __global__ void __launch_bounds__(256) k_chunks(int64_t n_seg, int64_t n_chunks,
     if (c == n_chunks - 1) chunk_seg[n_chunks] = n_seg;
     const int64_t w = work_pre[g1] - work_pre[g0];
     chunk_cap[c] = ((w + (w >> 2)) >> kG) + 16;
-}
-
-// packed per-segment records for the sampler (one 64/96-byte read instead of eight gathers)
-__global__ void __launch_bounds__(256) k_pack(int model, int64_t n_seg, SegArrays sa, const double *__restrict__ kappa_s,
-                                              const int32_t *__restrict__ perm, const double *__restrict__ y_s,
-                                              const double *__restrict__ ly_s, const int32_t *__restrict__ excl,
-                                              SegRec *__restrict__ rec)
-{
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n_seg) return;
-    const int4 sg = sa.seg[g];
-    SegRec r;
-    r.u = sg.x;
-    r.a = sg.y;
-    r.b = sg.z;
-    r.sigma = sg.w;
-    r.h0 = sa.h0[g];
-    r.x0 = sa.x0[g];
-    r.d0 = sa.d0[g];
-    r.ku = kappa_s[sg.x];
-    r.id_u = perm[sg.x];
-    r.excl = excl ? excl[sg.x] : -1;
-    r.pad1 = r.pad2 = 0;
-    r.yu = model == FM_ECM ? y_s[sg.x] : 0.0;
-    r.ly_u = model == FM_ECM ? ly_s[sg.x] : 0.0;
-    r.omT = sa.omT[g];
-    r.iomT = sa.iomT[g];
-    rec[g] = r;
 }
 
 // the sampler's per-candidate gather record (Plan::cand)

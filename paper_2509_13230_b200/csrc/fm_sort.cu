@@ -9,8 +9,9 @@
 // histograms of all positions come with the keys from k_validate_key).  A pass kernel takes tiles in ticket order (atomic counter),
 // ranks its 2048 keys stably (warp __match_any_sync ranks + cross-warp prefix in shared
 // memory), publishes its per-digit counts and resolves its global offsets by decoupled
-// look-back over the preceding tiles (64-bit status words: 2 flag bits + 62-bit count), then
-// scatters.  Each pass reads and writes the keys once (24 B per key).
+// look-back over the preceding tiles (64-bit status words: 2 flag bits + 62-bit count), stages
+// the tile in digit order in shared memory and writes each digit run contiguously (coalesced).
+// Each pass reads and writes the keys once (24 B per key).
 #include "fm_internal.cuh"
 
 namespace fm {
@@ -36,9 +37,13 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
                                                    uint64_t *status, unsigned int *tile_counter)
 {
     __shared__ int wcnt[kThreads / 32][kRadix];
-    __shared__ int64_t s_base[kRadix];
+    __shared__ int64_t s_base[kRadix];   // global position of the tile's first key of each digit
+    __shared__ int s_lstart[kRadix];     // tile-local position of the tile's first key of each digit
     __shared__ unsigned int s_wsum[kThreads / 32];
+    __shared__ int s_wtot[kThreads / 32];
     __shared__ unsigned int s_tile;
+    __shared__ uint64_t s_key[kTile];    // the tile in digit order (stable): coalesced global writes
+    __shared__ int32_t s_val[kTile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int w = 0; w < kThreads / 32; w++) wcnt[w][threadIdx.x] = 0;
@@ -56,6 +61,7 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     const int64_t tile = s_tile;
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t wbase = tile * kTile + (int64_t)wid * (kTile / (kThreads / 32));
+    const int nvalid = (int)min((int64_t)kTile, n - tile * kTile);
     uint64_t key[kItems];
     int32_t val[kItems];
     int dig[kItems], loc[kItems];
@@ -76,9 +82,9 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     }
     __syncthreads();
     // thread d: tile-local prefix over warps, the tile's count of digit d, and its global base
+    int acc = 0;
     {
         const int d = threadIdx.x;
-        int acc = 0;
         for (int w = 0; w < kThreads / 32; w++) {
             const int c = wcnt[w][d];
             wcnt[w][d] = acc;
@@ -110,13 +116,40 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
         }
         s_base[d] = (int64_t)(dbase + prefix);
     }
+    // tile-local exclusive scan of the digit counts (block-wide over the 256 digits)
+    {
+        int inc2 = acc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc2, o);
+            if (lane >= o) inc2 += t;
+        }
+        if (lane == 31) s_wtot[wid] = inc2;
+        __syncthreads();
+        int off = inc2 - acc;
+        for (int w = 0; w < wid; w++) off += s_wtot[w];
+        s_lstart[threadIdx.x] = off;
+    }
     __syncthreads();
+    // stage the tile in digit order, then write it out contiguously per digit run
 #pragma unroll
     for (int r = 0; r < kItems; r++) {
         if (dig[r] < kRadix) {
-            const int64_t dst = s_base[dig[r]] + wcnt[wid][dig[r]] + loc[r];
-            kout[dst] = key[r];
-            vout[dst] = val[r];
+            const int p = s_lstart[dig[r]] + wcnt[wid][dig[r]] + loc[r];
+            s_key[p] = key[r];
+            s_val[p] = val[r];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kItems; r++) {
+        const int p = r * kThreads + threadIdx.x;
+        if (p < nvalid) {
+            const uint64_t k = s_key[p];
+            const int d = (int)((k >> shift) & 0xFF);
+            const int64_t dst = s_base[d] + (p - s_lstart[d]);
+            kout[dst] = k;
+            vout[dst] = s_val[p];
         }
     }
 }
