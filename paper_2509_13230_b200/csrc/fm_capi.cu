@@ -342,10 +342,13 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
         CK(cudaGetLastError(), "k_excl");
     }
 
-    if (model == FM_ECM)
+    // packed gather records: ECM always; UBCM when kappa + perm (12 B per candidate) would not stay
+    // resident in L2 (FM_UBCM_CAND_MIN candidates, default 2^21: 24 MB)
+    const bool want_cand = model == FM_ECM || n2 >= env_i64("FM_UBCM_CAND_MIN", int64_t(1) << 21);
+    if (want_cand)
         CK(cudaMallocAsync((void **)&p->cand, sizeof(double2) * kCandWords(model) * std::max<int64_t>(n2, 1), st),
            "alloc cand");
-    if (model == FM_ECM && n2 > 0) {
+    if (want_cand && n2 > 0) {
         count_launch();
         k_pack_cand<<<grid_for(n2, 256), 256, 0, st>>>((int)model, n2, p->ckappa, p->cperm, p->cy, p->cly, p->cand);
         CK(cudaGetLastError(), "k_pack_cand");
@@ -388,10 +391,23 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
     CK(cudaMallocAsync((void **)&p->rec, sizeof(SegRec) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
     if (n_seg > 0) {
+        // segment -> row map for large plans: exclusive scan of the row-start flags (small plans:
+        // a per-block search in k_emit, two launches fewer)
+        int64_t *seg_row_x = nullptr;
+        if (n_seg >= (int64_t(1) << 20)) {
+            CK(tmp.get(&seg_row_x, n_seg + 1), "alloc seg rows");
+            CK(cudaMemsetAsync(seg_row_x, 0, sizeof(int64_t) * (n_seg + 1), st), "memset seg rows");
+            count_launch();
+            k_row_starts<<<grid_for(n1, 256), 256, 0, st>>>(n1, row_m, seg_row_x);
+            const size_t rb = scan_tmp_bytes(n_seg + 1);
+            char *work_r;
+            CK(tmp.get(&work_r, rb), "alloc scan tmp");
+            CK(scan_exclusive_i64(seg_row_x, seg_row_x, n_seg, work_r, rb, st), "scan row starts");
+        }
         count_launch();
         k_emit<<<grid_for(n_seg, 256), 256, 0, st>>>((int)model, (int)kind, n1, nc, n_seg, p->kappa_s, p->y_s,
                                                      p->ly_s, p->perm, p->excl, p->ckappa, p->ymax, P, sc, rows,
-                                                     row_m, p->rec, seg_work);
+                                                     row_m, seg_row_x, p->rec, seg_work);
         CK(cudaGetLastError(), "k_emit");
     }
     {

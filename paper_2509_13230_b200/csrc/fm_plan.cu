@@ -204,78 +204,104 @@ __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, in
                                               const int32_t *__restrict__ excl, const double *__restrict__ ckappa,
                                               const double *__restrict__ ymax, const uint64_t *__restrict__ P,
                                               PlanScalars *sc, const RowInfo *__restrict__ rows,
-                                              const int64_t *__restrict__ row_seg, SegRec *__restrict__ rec,
+                                              const int64_t *__restrict__ row_seg,
+                                              const int64_t *__restrict__ seg_row_x, SegRec *__restrict__ rec,
                                               int64_t *__restrict__ seg_work)
 {
+    __shared__ __align__(16) SegRec s_rec[256];  // the block's records, written out coalesced
     __shared__ int64_t s_u0;
     const int64_t g0 = (int64_t)blockIdx.x * blockDim.x;
     const int64_t g = g0 + threadIdx.x;
+    const int nb = (int)min((int64_t)blockDim.x, n_seg - g0);  // records of this block
     // row u of segment g: largest u with row_seg[u] <= g.  Every row that has candidates has >= 1
-    // segment (rows with candidates: n-1 undirected, all n otherwise), so u(g) lies in
-    // [g - extra, g]; the block's first row u0 is found once, then u(g) in [u0, u0 + (g - g0)]
+    // segment (rows with candidates: n-1 undirected, all n otherwise).  Large plans: the number of
+    // row starts at or before g, minus one (seg_row_x = exclusive scan of the row-start flags);
+    // small plans (seg_row_x NULL, fewer launches): u(g) in [g - extra, g], the block's first row
+    // u0 found once, then u(g) in [u0, u0 + (g - g0)]
     const int64_t rows_w = kind == FM_UNDIRECTED ? n - 1 : n;
-    const int64_t extra = n_seg - rows_w;
-    if (threadIdx.x == 0) {
-        int64_t lo = g0 - extra > 0 ? g0 - extra : 0, hi = g0 < rows_w - 1 ? g0 : rows_w - 1;
-        while (lo < hi) {
-            const int64_t mid = lo + ((hi - lo + 1) >> 1);
-            if (row_seg[mid] <= g0) lo = mid; else hi = mid - 1;
+    if (!seg_row_x) {
+        const int64_t extra = n_seg - rows_w;
+        if (threadIdx.x == 0) {
+            int64_t lo = g0 - extra > 0 ? g0 - extra : 0, hi = g0 < rows_w - 1 ? g0 : rows_w - 1;
+            while (lo < hi) {
+                const int64_t mid = lo + ((hi - lo + 1) >> 1);
+                if (row_seg[mid] <= g0) lo = mid; else hi = mid - 1;
+            }
+            s_u0 = lo;
         }
-        s_u0 = lo;
+        __syncthreads();
+    }
+    if (g < n_seg) {
+        const int F = sc->F;
+        int64_t u;
+        if (seg_row_x) {
+            u = seg_row_x[g + 1] - 1;
+        } else {
+            int64_t lo = s_u0, hi = s_u0 + (g - g0) < rows_w - 1 ? s_u0 + (g - g0) : rows_w - 1;
+            while (lo < hi) {
+                const int64_t mid = lo + ((hi - lo + 1) >> 1);
+                if (row_seg[mid] <= g) lo = mid; else hi = mid - 1;
+            }
+            u = lo;
+        }
+        const int64_t c0 = row_c0(kind, u);
+        const int64_t sigma = g - row_seg[u];
+        const int64_t m = row_seg[u + 1] - row_seg[u];
+        const RowInfo ri = rows[u];
+        int64_t a, b;
+        a = sigma == 0 ? c0 : plan_cut(P, F, nc, c0, ri, m, sigma);
+        b = sigma == m - 1 ? nc : plan_cut(P, F, nc, c0, ri, m, sigma + 1);
+        if (!(a < b) || !(a >= c0)) atomicOr(&sc->flags, kErrState);
+        SegRec r;
+        r.u = (int)u;
+        r.a = (int)a;
+        r.b = (int)b;
+        r.sigma = (int)sigma;
+        // bound at the virtual previous position a-1 (R3); a bipartite row start uses candidate 0 (R16)
+        const int64_t bp = a > 0 ? a - 1 : 0;
+        const double ku = kappa_s[u];
+        const double kq = __dmul_rn(ku, ckappa[bp]);
+        r.x0 = kq;
+        r.ku = ku;
+        r.id_u = perm[u];
+        r.excl = excl ? excl[u] : -1;
+        r.pad1 = r.pad2 = 0;
+        if (model == FM_UBCM) {
+            r.omT = 1.0;
+            r.iomT = 1.0;
+            r.d0 = __dadd_rn(1.0, kq);
+            r.h0 = log1p(kq);
+            r.yu = 0.0;
+            r.ly_u = 0.0;
+        } else {
+            const double T = __dmul_rn(y_s[u], ymax[a]);
+            const double omT = __dsub_rn(1.0, T);
+            const double iomT = __ddiv_rn(1.0, omT);
+            r.omT = omT;
+            r.iomT = iomT;
+            r.d0 = __dadd_rn(omT, kq);
+            r.h0 = log1p(__dmul_rn(kq, iomT));
+            r.yu = y_s[u];
+            r.ly_u = ly_s[u];
+        }
+        s_rec[threadIdx.x] = r;
+        const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, c0, ri.r, ri.sat, a);
+        const int64_t wb = plan_W(P, F, c0, ri.r, ri.sat, b);
+        seg_work[g] = wb - wa + kUnit;
     }
     __syncthreads();
-    if (g >= n_seg) return;
-    const int F = sc->F;
-    int64_t lo = s_u0, hi = s_u0 + (g - g0) < rows_w - 1 ? s_u0 + (g - g0) : rows_w - 1;
-    while (lo < hi) {
-        const int64_t mid = lo + ((hi - lo + 1) >> 1);
-        if (row_seg[mid] <= g) lo = mid; else hi = mid - 1;
-    }
-    const int64_t u = lo;
-    const int64_t c0 = row_c0(kind, u);
-    const int64_t sigma = g - row_seg[u];
-    const int64_t m = row_seg[u + 1] - row_seg[u];
-    const RowInfo ri = rows[u];
-    int64_t a, b;
-    a = sigma == 0 ? c0 : plan_cut(P, F, nc, c0, ri, m, sigma);
-    b = sigma == m - 1 ? nc : plan_cut(P, F, nc, c0, ri, m, sigma + 1);
-    if (!(a < b) || !(a >= c0)) atomicOr(&sc->flags, kErrState);
-    SegRec r;
-    r.u = (int)u;
-    r.a = (int)a;
-    r.b = (int)b;
-    r.sigma = (int)sigma;
-    // bound at the virtual previous position a-1 (R3); a bipartite row start uses candidate 0 (R16)
-    const int64_t bp = a > 0 ? a - 1 : 0;
-    const double ku = kappa_s[u];
-    const double kq = __dmul_rn(ku, ckappa[bp]);
-    r.x0 = kq;
-    r.ku = ku;
-    r.id_u = perm[u];
-    r.excl = excl ? excl[u] : -1;
-    r.pad1 = r.pad2 = 0;
-    if (model == FM_UBCM) {
-        r.omT = 1.0;
-        r.iomT = 1.0;
-        r.d0 = __dadd_rn(1.0, kq);
-        r.h0 = log1p(kq);
-        r.yu = 0.0;
-        r.ly_u = 0.0;
-    } else {
-        const double T = __dmul_rn(y_s[u], ymax[a]);
-        const double omT = __dsub_rn(1.0, T);
-        const double iomT = __ddiv_rn(1.0, omT);
-        r.omT = omT;
-        r.iomT = iomT;
-        r.d0 = __dadd_rn(omT, kq);
-        r.h0 = log1p(__dmul_rn(kq, iomT));
-        r.yu = y_s[u];
-        r.ly_u = ly_s[u];
-    }
-    rec[g] = r;
-    const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, c0, ri.r, ri.sat, a);
-    const int64_t wb = plan_W(P, F, c0, ri.r, ri.sat, b);
-    seg_work[g] = wb - wa + kUnit;
+    // 16-byte words of the block's records, consecutive threads -> consecutive addresses
+    const int4 *src = reinterpret_cast<const int4 *>(s_rec);
+    int4 *dst = reinterpret_cast<int4 *>(rec + g0);
+    constexpr int kWords = (int)(sizeof(SegRec) / 16);
+    for (int i = threadIdx.x; i < nb * kWords; i += blockDim.x) dst[i] = src[i];
+}
+
+// row-start flags for k_emit's segment -> row map: flag[row_seg[u]] = 1 for rows with segments
+__global__ void k_row_starts(int64_t n, const int64_t *__restrict__ row_seg, int64_t *__restrict__ flag)
+{
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n && row_seg[u + 1] > row_seg[u]) flag[row_seg[u]] = 1;
 }
 
 // directed (R16): excl[u] = candidate rank of row u's own node (inverse of the candidate order)

@@ -45,7 +45,9 @@ __global__ void k_rows(int model, int kind, int64_t n, int64_t nc, int64_t S, co
 __global__ void k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg, const double *kappa_s,
                        const double *y_s, const double *ly_s, const int32_t *perm, const int32_t *excl,
                        const double *ckappa, const double *ymax, const uint64_t *P, PlanScalars *sc,
-                       const RowInfo *rows, const int64_t *row_seg, SegRec *rec, int64_t *seg_work);
+                       const RowInfo *rows, const int64_t *row_seg, const int64_t *seg_row_x, SegRec *rec,
+                       int64_t *seg_work);
+__global__ void k_row_starts(int64_t n, const int64_t *row_seg, int64_t *flag);
 __global__ void k_rank_of(int64_t nc, const int32_t *cperm, int32_t *crank);
 __global__ void k_excl(int64_t n, const int32_t *perm, const int32_t *crank, int32_t *excl);
 __global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg,

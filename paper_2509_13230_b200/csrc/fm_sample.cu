@@ -315,7 +315,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         lyv[c] = v1.x;
                         id_v[c] = __double2loint(v1.y);
                         if (kRefresh) ymn[c] = __ldg(A.ymax_c + cur[c] + 1);
-                    } else {  // (UBCM: two plain gathers measured faster than the 16-byte record)
+                    } else if (A.cand) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
+                        const double2 v0 = __ldg(A.cand + (uint32_t)cur[c]);
+                        kv[c] = v0.x;
+                        id_v[c] = __double2loint(v0.y);
+                    } else {  // UBCM, L2-resident arrays: two plain gathers (measured no slower)
                         kv[c] = A.kappa_s[cur[c]];
                         id_v[c] = A.perm[cur[c]];
                     }

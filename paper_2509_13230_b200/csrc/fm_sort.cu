@@ -18,7 +18,10 @@ namespace fm {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+#ifndef FM_SORT_ITEMS
+#define FM_SORT_ITEMS 8
+#endif
+constexpr int kItems = FM_SORT_ITEMS;
 constexpr int kTile = kThreads * kItems;  // 2048 keys per tile, 256 per warp
 constexpr int kRadix = 256;
 constexpr int kPasses = 8;
