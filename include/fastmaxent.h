@@ -197,7 +197,9 @@ fm_status fm_timing_get(fm_timing *t, int reset);
 
 /* Diagnostics of the device math (tests only): out[i] = f(in[i]) for i < n on DEVICE buffers,
  * fn 0 = log(x) (x > 0 normal), 1 = log1p(x) (x >= 0), 2 = -log(u01(k)), k = (uint32) in[i]
- * -- the fp64 logarithms the sampler uses in place of libm. Stream-ordered. */
+ * -- the fp64 logarithms the sampler uses in place of libm; fn 3 = in[2i] / in[2i+1]
+ * by the sampler's Markstein division (in holds 2n doubles; must equal the IEEE quotient).
+ * Stream-ordered. */
 fm_status fm_debug_eval(int32_t fn, int64_t n, const double *in_dev, double *out_dev, void *cuda_stream);
 
 /* Release an fm_plan* or the buffers of an fm_edges* (the struct itself is caller-owned and

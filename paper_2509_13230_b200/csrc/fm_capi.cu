@@ -907,7 +907,7 @@ fm_status fm_plan_export_candidates(const fm_plan *plan, int32_t *cperm, double 
 
 fm_status fm_debug_eval(int32_t fn, int64_t n, const double *in_dev, double *out_dev, void *cuda_stream)
 {
-    if (fn < 0 || fn > 2 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return fail(FM_ERR_INVALID, "bad debug_eval args");
+    if (fn < 0 || fn > 3 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return fail(FM_ERR_INVALID, "bad debug_eval args");
     CK(launch_debug_eval(fn, n, in_dev, out_dev, (cudaStream_t)cuda_stream), "debug eval");
     return FM_OK;
 }

@@ -26,7 +26,8 @@ struct __align__(16) SegRec {
     int32_t u, a, b, sigma;  // focal rank, candidates [a, b), segment index in the row
     double h0, x0;           // initial bound at a-1: q0 = x0 / d0, h0 = -log(1 - q0)
     double d0, ku;           // ..., kappa_s[u]
-    int32_t id_u, excl, pad1, pad2;  // perm[u]; directed: candidate rank of u's own node, else -1
+    int32_t id_u, excl;      // perm[u]; directed: candidate rank of u's own node, else -1
+    double rh0;              // RN(1 / h0): the sampler divides E / h by Markstein's correction
     double yu, ly_u;         // ECM: y_s[u], log y_s[u]
     double omT, iomT;        // ECM: 1 - T, RN(1 / (1 - T))
 };

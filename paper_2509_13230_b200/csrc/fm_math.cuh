@@ -10,13 +10,13 @@
 // Method (table-driven, a textbook scheme; own constants):  x = 2^k z, z in [0.6875, 1.375),
 // i = 7 mantissa bits of z -> 128 subintervals with centres c_i, except the two subintervals
 // touching 1 which use c = 1 exactly (so log is relatively accurate near 1).  With
-// invc_i = RN(1/c_i) and logc_i = -log(invc_i) (computed once on the host in long double and
-// split as logc_hi, a multiple of 2^-43 like k * LN2_HI, plus logc_lo):  log x = k ln2 + logc_i + log1p(r),  r = z invc_i - 1 held exactly as
-// r_hi + r_lo (DMUL + FMA; Sterbenz), |r| < 2^-7, log1p(r) = r + r^2 P(r) with the degree-8
-// Taylor polynomial (truncation < 2^-59 relative).  k LN2_HI + logc_hi is exact and Fast2Sum
-// keeps its sum with r exact; the small terms are added last.
-// log1p(X) = log(u) + c/u with u = 1 + X and c its exact rounding error (TwoSum); 1/u is taken
-// as 2^-k invc (1 - r), whose relative error r^2 < 2^-14 is harmless on a term below 2^-53 u.
+// invc_i = RN(1/c_i) and logc_i = RN(-log(invc_i)) (computed once on the host in long double):
+// log x = k ln2 + logc_i + log1p(r),  r = RN(z invc_i - 1) (one FMA), |r| < 2^-7, and
+// log1p(r) = r + r^2 P(r) with the degree-6 Taylor polynomial P (truncation < 2^-59 relative).
+// Error budget (no double-word arithmetic): logc and the three final roundings,
+// <= ~2 ulp -- within the 2e-14 (~100 ulp) a custom log may have.
+// log1p(X) = log(u) + c/u with u = RN(1 + X) and c its exact rounding error (TwoSum): the
+// correction enters as r += c 2^-k invc (= c/u to first order, since 1 + r ~ z invc).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -26,8 +26,7 @@ namespace fm {
 constexpr int kLogTable = 128;
 
 struct LogTable {
-    double2 ic[kLogTable];      // (invc, logc_hi); logc_hi is a multiple of 2^-43 (see below)
-    double logc_lo[kLogTable];  // logc - logc_hi (|.| < 2^-44)
+    double2 ic[kLogTable];  // (invc, logc)
 };
 
 // polynomial coefficients and ln2 split (compile-time constants: materialised as immediates)
@@ -55,13 +54,15 @@ __device__ __forceinline__ double fm_log_core(double x, double c, const Tab &T)
     const double z = __longlong_as_double((long long)(ix - (tmp & 0xfff0000000000000ull)));
     // (double)k without a conversion instruction: 2^52 + (k + 2^20) - (2^52 + 2^20), exact
     const double kd = __dsub_rn(__hiloint2double(0x43300000, (int)(k + 0x100000)), 0x1p52 + 0x1p20);
-    double invc, lc_hi, lc_lo;
-    T.entry(i, invc, lc_hi, lc_lo);
+    double invc, logc;
+    T.entry(i, invc, logc);
     const LogConsts &K = T.C();
-    // r = z * invc - 1 exactly, as r + p_lo
-    const double p_hi = __dmul_rn(z, invc);
-    const double p_lo = __fma_rn(z, invc, -p_hi);
-    const double r = __dsub_rn(p_hi, 1.0);
+    double r = __fma_rn(z, invc, -1.0);
+    if (kCorr) {  // + c/x = c 2^-k invc / (1 + r) -> r += c 2^-k invc
+        const int64_t kc = k < 1000 ? k : 1000;  // beyond, c/x < 2^-1000 of the result: irrelevant
+        const double sc = __longlong_as_double((long long)((uint64_t)(1023 - kc) << 52));
+        r = __dadd_rn(r, __dmul_rn(__dmul_rn(c, invc), sc));
+    }
     const double r2 = __dmul_rn(r, r);
     // P(r) = -1/2 + r/3 - r^2/4 + r^3/5 - r^4/6 + r^5/7 - r^6/8  (Estrin)
     const double e01 = __fma_rn(r, K.c3, -0.5);
@@ -70,23 +71,9 @@ __device__ __forceinline__ double fm_log_core(double x, double c, const Tab &T)
     const double e46 = __fma_rn(r2, -0.125, e45);
     const double r4 = __dmul_rn(r2, r2);
     const double P = __fma_rn(r4, e46, __fma_rn(r2, e23, e01));
-    // correction c/x = c 2^-k invc (1 - r)
-    double corr = 0.0;
-    if (kCorr) {
-        const int64_t kc = k < 1000 ? k : 1000;  // beyond, c/x < 2^-1000 of the result: irrelevant
-        const double sc = __longlong_as_double((long long)((uint64_t)(1023 - kc) << 52));
-        corr = __dmul_rn(__dmul_rn(c, invc), __dmul_rn(sc, __dsub_rn(1.0, r)));
-    }
-    // leading terms exactly: s = k ln2_hi + logc_hi is exact (both multiples of 2^-43, |s| < 2^10),
-    // hi + lo1 = s + r (Fast2Sum, |s| >= |r| or s = 0)
-    const double s = __fma_rn(kd, K.ln2_hi, lc_hi);
-    const double hi = __dadd_rn(s, r);
-    const double lo1 = __dsub_rn(r, __dsub_rn(hi, s));
-    double lo = __fma_rn(kd, K.ln2_lo, kCorr ? __dadd_rn(lc_lo, corr) : lc_lo);
-    lo = __dadd_rn(lo, p_lo);
-    lo = __dadd_rn(lo, lo1);
-    lo = __fma_rn(r2, P, lo);
-    return __dadd_rn(hi, lo);
+    const double t = __fma_rn(kd, K.ln2_hi, logc);                 // k ln2_hi exact (|k| < 2^11)
+    const double s = __fma_rn(kd, K.ln2_lo, __fma_rn(r2, P, r));  // log1p(r) + k ln2_lo
+    return __dadd_rn(t, s);
 }
 
 // log(x), x > 0 finite normal
@@ -105,6 +92,18 @@ __device__ __forceinline__ double fm_log1p(double X, const Tab &T)
     const double b1 = __dsub_rn(u, a1);  // the part of u that came from X
     const double c = __dadd_rn(__dsub_rn(1.0, a1), __dsub_rn(X, b1));
     return fm_log_core<true>(u, c, T);
+}
+
+// RN(a / b) from y = RN(1 / b) (Markstein's theorem): q0 = RN(a y) is within one ulp of a / b,
+// the FMA residual r = a - b q0 is exact, and RN(q0 + r y) = RN(a / b) -- the IEEE quotient,
+// for operands whose intermediates neither overflow nor underflow (the sampler: a = E in
+// [2^-33, 23], b = h > 0; b = 0 gives y = inf and a NaN, which fails every "R <" test like the
+// quotient +inf does)
+__device__ __forceinline__ double div_markstein(double a, double b, double y)
+{
+    const double q0 = __dmul_rn(a, y);
+    const double r = __fma_rn(-b, q0, a);
+    return __fma_rn(r, y, q0);
 }
 
 }  // namespace fm

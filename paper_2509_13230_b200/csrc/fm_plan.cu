@@ -265,7 +265,6 @@ __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, in
         r.ku = ku;
         r.id_u = perm[u];
         r.excl = excl ? excl[u] : -1;
-        r.pad1 = r.pad2 = 0;
         if (model == FM_UBCM) {
             r.omT = 1.0;
             r.iomT = 1.0;
@@ -284,6 +283,7 @@ __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, in
             r.yu = y_s[u];
             r.ly_u = ly_s[u];
         }
+        r.rh0 = __drcp_rn(r.h0);
         s_rec[threadIdx.x] = r;
         const int64_t wa = sigma == 0 ? 0 : plan_W(P, F, c0, ri.r, ri.sat, a);
         const int64_t wb = plan_W(P, F, c0, ri.r, ri.sat, b);

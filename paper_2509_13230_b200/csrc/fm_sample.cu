@@ -34,33 +34,26 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kBatch = 64;  // tasks per warp batch
 
-// per-block copy of the log table: (invc, logc_hi) pairs then logc_lo, structure of arrays (a
-// 32-byte array-of-structures entry doubles the bank conflicts of the random lookups)
+// per-block copy of the log table: (invc, logc) pairs, one 16-byte lookup
 struct LogSmem {
     double2 ic[kLogTable];
-    double lo[kLogTable];
 };
 __shared__ __align__(16) LogSmem s_log;
 struct SmemLogTab {
     const LogConsts &lc;  // in the kernel's parameter bank: constant-bank operands, no register copies
     uint32_t base;        // 32-bit shared address of s_log (opaque: one register, no per-use address math)
-    __device__ __forceinline__ void entry(int i, double &invc, double &hi, double &lo) const
+    __device__ __forceinline__ void entry(int i, double &invc, double &logc) const
     {
-        asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(invc), "=d"(hi) : "r"(base + ((uint32_t)i << 4)));
-        asm("ld.shared.f64 %0, [%1+2048];" : "=d"(lo) : "r"(base + ((uint32_t)i << 3)));
+        asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(invc), "=d"(logc) : "r"(base + ((uint32_t)i << 4)));
     }
     __device__ __forceinline__ const LogConsts &C() const { return lc; }
 };
-static_assert(sizeof(double2) * kLogTable == 2048, "lo offset in SmemLogTab::entry");
 
 // fill s_log; returns its shared address, produced after the barrier (so no table read is
 // scheduled before the table is complete)
 __device__ __forceinline__ uint32_t load_logtab()
 {
-    for (int j = threadIdx.x; j < kLogTable; j += blockDim.x) {
-        s_log.ic[j] = g_logtab.ic[j];
-        s_log.lo[j] = g_logtab.logc_lo[j];
-    }
+    for (int j = threadIdx.x; j < kLogTable; j += blockDim.x) s_log.ic[j] = g_logtab.ic[j];
     __syncthreads();
     uint32_t base = (uint32_t)__cvta_generic_to_shared(&s_log);
     asm volatile("mov.b32 %0, %0;" : "+r"(base));
@@ -71,7 +64,9 @@ __device__ __forceinline__ uint32_t load_logtab()
 // parallelism (instantiated with kC = 1: two chains measured slower, their registers cost more
 // occupancy than their ILP gains).
 // kStats: statistics mode (fm_sample_degrees): degree / strength sums instead of edge lists.
-template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh>
+// kCand: UBCM gathers one 16-byte (kappa, id) record (large N) instead of two arrays.
+// kOrdered: bipartite / directed output (row id, candidate id) as is (R16).
+template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, bool kCand, bool kOrdered>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
@@ -99,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     uint32_t row_acc[kC];          // statistics mode: accepted edges of the current segment
     unsigned long long row_w[kC];  //                  and their weight sum (ECM)
     uint32_t sg[kC], d[kC], wacc[kC], wwt[kC];
-    double xq[kC], dq[kC], h[kC], ku[kC], E[kC], yu[kC], lyu[kC], omT[kC], iomT[kC];
+    double xq[kC], dq[kC], h[kC], rh[kC], ku[kC], E[kC], yu[kC], lyu[kC], omT[kC], iomT[kC];
 #pragma unroll
     for (int c = 0; c < kC; c++) {
         s_task[threadIdx.x * kC + c] = -1;
@@ -113,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         row_acc[c] = 0;
         row_w[c] = 0;
         sg[c] = d[c] = wacc[c] = wwt[c] = 0;
-        xq[c] = 0.0; dq[c] = 1.0; h[c] = 0.0; ku[c] = 0.0; E[c] = 0.0;
+        xq[c] = 0.0; dq[c] = 1.0; h[c] = 0.0; rh[c] = 0.0; ku[c] = 0.0; E[c] = 0.0;
         yu[c] = 0.0; lyu[c] = 0.0; omT[c] = 1.0; iomT[c] = 1.0;
     }
     // draws; landed = draws - segments and accepted = edges are derived by the host (every
@@ -163,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         ku[c] = p2.y;
         id_u[c] = p3.x;
         excl[c] = p3.y;  // directed: u's own in-copy (R16), else -1
+        rh[c] = __hiloint2double(p3.w, p3.z);
         if (kModel == FM_ECM) {
             yu[c] = p4.x;
             lyu[c] = p4.y;
@@ -289,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             }
             if (act[c] && !fresh[c]) {
                 n_draw++;
-                const double R = __ddiv_rn(E[c], h[c]);
+                const double R = div_markstein(E[c], h[c], rh[c]);  // = E / h, IEEE
                 // R < lim (lim = b-1-cur >= 0 an integer) <=> R < 2^31 and floor(R) < lim, with
                 // floor(R) the low word of RZ(R + 2^52) (exact for 0 <= R < 2^52): no I2F / F2I
                 const double Rt = __dadd_rz(R, 0x1p52);
@@ -315,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         lyv[c] = v1.x;
                         id_v[c] = __double2loint(v1.y);
                         if (kRefresh) ymn[c] = __ldg(A.ymax_c + cur[c] + 1);
-                    } else if (A.cand) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
+                    } else if (kCand) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
                         const double2 v0 = __ldg(A.cand + (uint32_t)cur[c]);
                         kv[c] = v0.x;
                         id_v[c] = __double2loint(v0.y);
@@ -356,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         xq[c] = X;
                         dq[c] = D;
                         h[c] = hn;
+                        rh[c] = __drcp_rn(hn);
                     }
                 } else {
                     const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(us, 0.0))) : 1.0;
@@ -374,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         xq[c] = z;
                         dq[c] = __dadd_rn(omb, z);
                         h[c] = hn;
+                        rh[c] = __drcp_rn(hn);
                         if (acc[c]) {  // Eq. 5 weight, log t = log y_u + log y_v (R8)
                             const double lu = fm_log(U01(w_wt[c]), T);
                             const double G = floor(__ddiv_rn(lu, __dadd_rn(lyu[c], lyv[c])));
@@ -405,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 if (A.rank_hist) atomicAdd(&A.rank_hist[cur[c]], 1ull);
                 n_acc++;
             } else if (acc[c]) {
-                const int2 ev = A.ordered ? make_int2(id_u[c], id_v[c])
+                const int2 ev = kOrdered ? make_int2(id_u[c], id_v[c])
                                           : make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
                 if (cnt[c] < cap[c]) {
                     A.edges[slot[c] + cnt[c]] = ev;
@@ -552,13 +550,19 @@ __global__ void k_add_u64(const uint64_t *__restrict__ in, uint64_t *__restrict_
     if (i < n) out[i] += in[i];
 }
 
-// diagnostics: fn 0 = fm_log(x), 1 = fm_log1p(x), 2 = -fm_log(u01(k)) with k = (uint32)x
+// diagnostics: fn 0 = fm_log(x), 1 = fm_log1p(x), 2 = -fm_log(u01(k)) with k = (uint32)x,
+// 3 = in[2i] / in[2i+1] by div_markstein with the reciprocal the sampler uses
 __global__ void __launch_bounds__(256) k_debug_eval(int fn, int64_t n, const double *__restrict__ in,
                                                     double *__restrict__ out, const LogConsts lc)
 {
     const SmemLogTab T{lc, load_logtab()};
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (fn == 3) {
+        const double b = in[2 * i + 1];
+        out[i] = div_markstein(in[2 * i], b, __drcp_rn(b));
+        return;
+    }
     const double x = in[i];
     double y;
     if (fn == 0) y = fm_log(x, T);
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(256) k_debug_eval(int fn, int64_t n, const dou
     out[i] = y;
 }
 
-// host: the log table, computed once in long double (logc = -log(invc) to ~2^-64 relative)
+// host: the log table, computed once in long double (logc = RN(-log(invc)))
 LogTable make_log_table()
 {
     LogTable T;
@@ -577,10 +581,7 @@ LogTable make_log_table()
         else c = 1.0L + ((long double)(i - 80) + 0.5L) / 128.0L;     // z in [1, 1.375), width 1/128
         if (i == 79 || i == 80) c = 1.0L;                             // the two intervals touching 1
         const double invc = (double)(1.0L / c);
-        const long double L = -logl((long double)invc);
-        const double hi = (double)(roundl(L * 0x1p43L) * 0x1p-43L);  // multiple of 2^-43
-        T.ic[i] = make_double2(invc, hi);
-        T.logc_lo[i] = (double)(L - (long double)hi);
+        T.ic[i] = make_double2(invc, (double)(-logl((long double)invc)));
     }
     return T;
 }
@@ -604,35 +605,44 @@ cudaError_t ensure_log_table(cudaStream_t st)
     return e;
 }
 
-// one instantiation per (model, statistics mode, ECM bound refresh); kMinB = 3 blocks per SM
-template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh>
+// one instantiation per (model, statistics mode, ECM bound refresh, UBCM gather record, output
+// orientation); kMinB = 3 blocks per SM
+template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, bool kCand, bool kOrdered>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
+    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kCand, kOrdered>;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t dyn = (size_t)kThreads * kC * (kModel == FM_ECM ? 96 : 64);
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats, kRefresh>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)dyn);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         // shared-memory carveout (percent of the unified L1/shared capacity): the driver's default
         // picked 135 KB of shared memory for 3 x 27 KB of need; 40 % leaves more L1 for the kappa /
         // perm gathers (UBCM kernel -1 %; 0 % starves occupancy: +70 %).  FM_SAMPLE_CARVEOUT
         // overrides (-1 = driver default)
         const char *cv = getenv("FM_SAMPLE_CARVEOUT");
         const int carve = cv && *cv ? atoi(cv) : 40;
-        if (carve >= 0) cudaFuncSetAttribute(k_sample<kModel, kMinB, kC, kStats, kRefresh>,
-                                             cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+        if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         attr_set = true;
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sample<kModel, kMinB, kC, kStats, kRefresh>, kThreads, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
     int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
     const int64_t need = (a.n_tasks + kThreads * kC - 1) / (kThreads * kC);  // <= one task per chain at start
     if (need < blocks) blocks = need;
     count_launch();
-    k_sample<kModel, kMinB, kC, kStats, kRefresh><<<(unsigned)blocks, kThreads, dyn, st>>>(a);
+    kern<<<(unsigned)blocks, kThreads, dyn, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int kModel, bool kStats, bool kRefresh, bool kCand>
+static cudaError_t launch_sample_o(const SampleArgs &a, cudaStream_t st)
+{
+    // statistics mode writes no pairs: its orientation is irrelevant
+    if constexpr (!kStats)
+        if (a.ordered) return launch_sample_t<kModel, 3, 1, kStats, kRefresh, kCand, true>(a, st);
+    return launch_sample_t<kModel, 3, 1, kStats, kRefresh, kCand, false>(a, st);
 }
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
@@ -648,12 +658,15 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
     }
     // one chain per thread, 3 blocks of 256 per SM (kC = 2, 2 or 4 blocks per SM measured slower)
     const bool stats = a.deg_row != nullptr || a.rank_hist != nullptr;
-    if (model == FM_UBCM)
-        return stats ? launch_sample_t<FM_UBCM, 3, 1, true, false>(a, st)
-                     : launch_sample_t<FM_UBCM, 3, 1, false, false>(a, st);
-    if (stats) return launch_sample_t<FM_ECM, 3, 1, true, false>(a, st);
-    return a.ymax_c ? launch_sample_t<FM_ECM, 3, 1, false, true>(a, st)
-                    : launch_sample_t<FM_ECM, 3, 1, false, false>(a, st);
+    if (model == FM_UBCM) {
+        if (a.cand) return stats ? launch_sample_o<FM_UBCM, true, false, true>(a, st)
+                                 : launch_sample_o<FM_UBCM, false, false, true>(a, st);
+        return stats ? launch_sample_o<FM_UBCM, true, false, false>(a, st)
+                     : launch_sample_o<FM_UBCM, false, false, false>(a, st);
+    }
+    if (stats) return launch_sample_o<FM_ECM, true, false, false>(a, st);
+    return a.ymax_c ? launch_sample_o<FM_ECM, false, true, false>(a, st)
+                    : launch_sample_o<FM_ECM, false, false, false>(a, st);
 }
 
 cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *spill_off,

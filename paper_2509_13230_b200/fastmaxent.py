@@ -377,9 +377,11 @@ def timing_get(reset: bool = False) -> dict:
 
 
 def debug_eval(fn: int, x):
-    """fm_debug_eval: the device fp64 logarithms (0 log, 1 log1p, 2 -log(u01(k))) on a CUDA float64 tensor."""
+    """fm_debug_eval: the device fp64 logarithms (0 log, 1 log1p, 2 -log(u01(k))) on a CUDA float64 tensor;
+    fn 3: x of shape [n, 2] -> x[:, 0] / x[:, 1] by the sampler's Markstein division."""
     import torch
     x = x.to(device="cuda", dtype=torch.float64).contiguous()
-    out = torch.empty_like(x)
-    _check(lib.fm_debug_eval(int(fn), x.numel(), C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), _stream(None)))
+    n = x.numel() // 2 if fn == 3 else x.numel()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _check(lib.fm_debug_eval(int(fn), n, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), _stream(None)))
     return out
