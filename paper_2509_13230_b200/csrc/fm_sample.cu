@@ -17,6 +17,7 @@
 // table-driven fm_log/fm_log1p (fm_math.cuh, ~0.5 ulp).
 #include <float.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -31,10 +32,20 @@ __device__ LogTable g_logtab;
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef FM_SAMPLE_THREADS
+#define FM_SAMPLE_THREADS 256
+#endif
+#ifndef FM_SAMPLE_MINB_UBCM
+#define FM_SAMPLE_MINB_UBCM 3
+#endif
+#ifndef FM_SAMPLE_MINB_ECM
+#define FM_SAMPLE_MINB_ECM 3
+#endif
+constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
 constexpr int kBatch = 64;  // tasks per warp batch
 
-// per-block copy of the log table: (invc, logc) pairs, one 16-byte lookup
+// per-block copy of the log table: (invc, logc) pairs, one 16-byte lookup (8 conflict-free
+// copies, one per bank group, measured no faster: the lookups are not the bottleneck)
 struct LogSmem {
     double2 ic[kLogTable];
 };
@@ -49,8 +60,8 @@ struct SmemLogTab {
     __device__ __forceinline__ const LogConsts &C() const { return lc; }
 };
 
-// fill s_log; returns its shared address, produced after the barrier (so no table read is
-// scheduled before the table is complete)
+// fill s_log; returns this lane's column address, produced after the barrier (so no table read
+// is scheduled before the table is complete)
 __device__ __forceinline__ uint32_t load_logtab()
 {
     for (int j = threadIdx.x; j < kLogTable; j += blockDim.x) s_log.ic[j] = g_logtab.ic[j];
@@ -73,7 +84,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // rarely used per-chain task state lives in shared memory (registers are the occupancy limit)
     __shared__ int64_t s_task[kThreads * kC];   // current task id, -1 none
     __shared__ int64_t s_spill[kThreads * kC];  // its spill region: -1 none, -2 failed
-    constexpr int kRecBytes = kModel == FM_ECM ? 96 : 64;  // bytes of SegRec the model reads
     const SmemLogTab T{A.lc, load_logtab()};
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
@@ -85,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     int64_t bpos = 0, bend = 0;
     bool warp_done = false;
     // ---- per-chain task state ----
-    int64_t slot[kC];
+    int2 *eb[kC];  // the task's output slot (scratch, or the final list when re-running)
     int32_t g[kC], g_end[kC], cnt[kC], cap[kC];
     uint32_t s_abs[kC];
     // ---- per-chain segment state ----
@@ -99,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     for (int c = 0; c < kC; c++) {
         s_task[threadIdx.x * kC + c] = -1;
         s_spill[threadIdx.x * kC + c] = -1;
-        slot[c] = 0;
+        eb[c] = A.edges;
         g[c] = g_end[c] = cnt[c] = cap[c] = 0;
         s_abs[c] = 0;
         act[c] = false;
@@ -119,10 +129,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // segment g[c] of chain c's task becomes current (64/96-byte record; the record of the next
     // segment is prefetched into this chain's shared-memory slot with cp.async)
     // this thread's prefetch slots: 32-bit shared addresses (no generic-address arithmetic)
-    uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(s_dyn) + threadIdx.x * kC * kRecBytes;
+    // structure of arrays: 16-byte part k of thread t's slot at (k * kThreads + t) * 16, so the
+    // 8 lanes of a 16-byte shared access touch 8 consecutive 16-byte words (conflict-free)
+    static_assert(kC == 1, "prefetch slot layout assumes one chain per thread");
+    constexpr int kPart = 16 * kThreads;
+    uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(s_dyn) + threadIdx.x * 16;
     asm volatile("mov.b32 %0, %0;" : "+r"(slot0));  // opaque: held in a register, not recomputed per use
     auto start_seg = [&](const int c, const bool prefetched) {
-        const uint32_t my_next = slot0 + c * kRecBytes;
+        const uint32_t my_next = slot0;
         int4 p0, p3;
         double2 p1, p2, p4, p5;
         if (prefetched) {
@@ -130,12 +144,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             uint32_t sa = my_next;
             asm volatile("cp.async.wait_all;\n" : "+r"(sa)::"memory");
             asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(p0.x), "=r"(p0.y), "=r"(p0.z), "=r"(p0.w) : "r"(sa));
-            asm("ld.shared.v2.f64 {%0,%1}, [%2+16];" : "=d"(p1.x), "=d"(p1.y) : "r"(sa));
-            asm("ld.shared.v2.f64 {%0,%1}, [%2+32];" : "=d"(p2.x), "=d"(p2.y) : "r"(sa));
-            asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4+48];" : "=r"(p3.x), "=r"(p3.y), "=r"(p3.z), "=r"(p3.w) : "r"(sa));
+            asm("ld.shared.v2.f64 {%0,%1}, [%2+%3];" : "=d"(p1.x), "=d"(p1.y) : "r"(sa), "n"(kPart));
+            asm("ld.shared.v2.f64 {%0,%1}, [%2+%3];" : "=d"(p2.x), "=d"(p2.y) : "r"(sa), "n"(2 * kPart));
+            asm("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4+%5];"
+                : "=r"(p3.x), "=r"(p3.y), "=r"(p3.z), "=r"(p3.w) : "r"(sa), "n"(3 * kPart));
             if (kModel == FM_ECM) {
-                asm("ld.shared.v2.f64 {%0,%1}, [%2+64];" : "=d"(p4.x), "=d"(p4.y) : "r"(sa));
-                asm("ld.shared.v2.f64 {%0,%1}, [%2+80];" : "=d"(p5.x), "=d"(p5.y) : "r"(sa));
+                asm("ld.shared.v2.f64 {%0,%1}, [%2+%3];" : "=d"(p4.x), "=d"(p4.y) : "r"(sa), "n"(4 * kPart));
+                asm("ld.shared.v2.f64 {%0,%1}, [%2+%3];" : "=d"(p5.x), "=d"(p5.y) : "r"(sa), "n"(5 * kPart));
             }
         } else {
             const SegRec *r = A.rec + g[c];
@@ -173,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             constexpr int parts = kModel == FM_ECM ? 6 : 4;
 #pragma unroll
             for (int k = 0; k < parts; k++)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(my_next + 16 * k), "l"(src + 16 * k)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(my_next + kPart * k), "l"(src + 16 * k)
                              : "memory");
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         }
@@ -196,12 +211,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     };
 
     for (;;) {
-        // ---- 1. task management: chains whose task has no segment left take the next task ids
-        //      of the warp's batch (the next batch is requested as soon as one is opened) ----
+        // ---- 1. task management (only when a chain of the warp has no segment left; a single
+        //      vote otherwise): such chains take the next task ids of the warp's batch (the next
+        //      batch is requested as soon as one is opened) ----
         bool fresh[kC];
+        bool need_any = false;
 #pragma unroll
         for (int c = 0; c < kC; c++) {
             fresh[c] = false;
+            need_any = need_any || !act[c];
+        }
+        if (__any_sync(0xffffffffu, need_any)) {
+#pragma unroll
+        for (int c = 0; c < kC; c++) {
             const bool needc = !act[c];
             const int ci = threadIdx.x * kC + c;
             if (needc) {
@@ -238,10 +260,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     g[c] = (int32_t)A.tm.seg[kk][ch];
                     g_end[c] = (int32_t)A.tm.seg[kk][ch + 1];
                     if (A.rerun_base) {
-                        slot[c] = A.rerun_base[t];
-                        cap[c] = (int32_t)max((int64_t)0, min((int64_t)INT32_MAX, A.out_cap - slot[c]));  // bounded by the list
+                        const int64_t sl = A.rerun_base[t];
+                        eb[c] = A.edges + sl;
+                        cap[c] = (int32_t)max((int64_t)0, min((int64_t)INT32_MAX, A.out_cap - sl));  // bounded by the list
                     } else {
-                        slot[c] = s * A.tm.cap_per_sample + A.tm.cap[kk][ch];
+                        eb[c] = A.edges + (s * A.tm.cap_per_sample + A.tm.cap[kk][ch]);
                         cap[c] = (int32_t)(A.tm.cap[kk][ch + 1] - A.tm.cap[kk][ch]);
                     }
                     s_abs[c] = A.first_sample + (uint32_t)s;
@@ -261,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         if (!__any_sync(0xffffffffu, any_act)) {
             if (warp_done) break;
             continue;
+        }
         }
         // ---- 2. a freshly fetched task consumes no draw this iteration: like a restarted chain,
         //      it only computes E of its draw 0 in the convergent block 4+5 ----
@@ -343,8 +367,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 // next draw, log1p of this candidate) stay independent; exact since us in (0,1)
                 // (kv is read only if landed: the ?: evaluates the selected operand only)
                 const double Enew = -fm_log(us, T);
+#ifdef FM_ELOG_FIRST
+                const double ord = Enew;  // the gathered kv is used after E of the next draw
+#else
+                const double ord = us;
+#endif
                 if (kModel == FM_UBCM) {
-                    const double X = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(us, 0.0))) : 1.0;
+                    const double X = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ord, 0.0))) : 1.0;
                     const double D = __dadd_rn(1.0, X);
                     const double hn = fm_log1p(X, T);
                     if (landed[c]) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
@@ -355,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         rh[c] = __drcp_rn(hn);
                     }
                 } else {
-                    const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(us, 0.0))) : 1.0;
+                    const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ord, 0.0))) : 1.0;
                     const double t = __dmul_rn(yu[c], yv[c]);  // (ECM: yv defined on every path, see above)
                     const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
                     // the bound for the candidates still ahead: per segment 1 - T = omT, or (kRefresh,
@@ -406,8 +435,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 const int2 ev = kOrdered ? make_int2(id_u[c], id_v[c])
                                           : make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
                 if (cnt[c] < cap[c]) {
-                    A.edges[slot[c] + cnt[c]] = ev;
-                    if (kModel == FM_ECM) A.weights[slot[c] + cnt[c]] = w[c];
+                    eb[c][cnt[c]] = ev;
+                    if (kModel == FM_ECM) A.weights[(eb[c] - A.edges) + cnt[c]] = w[c];
                 } else if (!A.rerun_base && cnt[c] < 2 * cap[c]) {  // spill: one extra region of `cap`
                     const int ci = threadIdx.x * kC + c;
                     int64_t sp = s_spill[ci];
@@ -622,8 +651,15 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         // picked 135 KB of shared memory for 3 x 27 KB of need; 40 % leaves more L1 for the kappa /
         // perm gathers (UBCM kernel -1 %; 0 % starves occupancy: +70 %).  FM_SAMPLE_CARVEOUT
         // overrides (-1 = driver default)
+        // (raised to what kMinB blocks need: static + dynamic shared memory + 1 KB reserved each)
         const char *cv = getenv("FM_SAMPLE_CARVEOUT");
-        const int carve = cv && *cv ? atoi(cv) : 40;
+        int carve = cv && *cv ? atoi(cv) : 40;
+        cudaFuncAttributes fa;
+        if (carve >= 0 && cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
+            const size_t need = (size_t)kMinB * (fa.sharedSizeBytes + dyn + 1024);
+            const int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+            carve = std::max(carve, std::min(pct, 100));
+        }
         if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
         attr_set = true;
     }
@@ -639,10 +675,11 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 template <int kModel, bool kStats, bool kRefresh, bool kCand>
 static cudaError_t launch_sample_o(const SampleArgs &a, cudaStream_t st)
 {
+    constexpr int kMinB = kModel == FM_ECM ? FM_SAMPLE_MINB_ECM : FM_SAMPLE_MINB_UBCM;
     // statistics mode writes no pairs: its orientation is irrelevant
     if constexpr (!kStats)
-        if (a.ordered) return launch_sample_t<kModel, 3, 1, kStats, kRefresh, kCand, true>(a, st);
-    return launch_sample_t<kModel, 3, 1, kStats, kRefresh, kCand, false>(a, st);
+        if (a.ordered) return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kCand, true>(a, st);
+    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kCand, false>(a, st);
 }
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
