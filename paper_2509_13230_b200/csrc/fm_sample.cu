@@ -75,9 +75,11 @@ __device__ __forceinline__ uint32_t load_logtab()
 // parallelism (instantiated with kC = 1: two chains measured slower, their registers cost more
 // occupancy than their ILP gains).
 // kStats: statistics mode (fm_sample_degrees): degree / strength sums instead of edge lists.
-// kCand: UBCM gathers one 16-byte (kappa, id) record (large N) instead of two arrays.
+// kGather (UBCM): 0 = kappa and id from two arrays, 1 = one 16-byte (kappa, id) record, 2 = kappa
+// only: the scratch edge holds (row id, candidate RANK) and the compaction maps the rank to its id
+// (the id gather leaves the latency-bound chain for the bandwidth-bound copy).
 // kOrdered: bipartite / directed output (row id, candidate id) as is (R16).
-template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, bool kCand, bool kOrdered>
+template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
@@ -335,7 +337,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         lyv[c] = v1.x;
                         id_v[c] = __double2loint(v1.y);
                         if (kRefresh) ymn[c] = __ldg(A.ymax_c + cur[c] + 1);
-                    } else if (kCand) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
+                    } else if (kGather == 2) {  // UBCM: κ only, the id is mapped in the compaction
+                        kv[c] = A.kappa_s[cur[c]];
+                    } else if (kGather == 1) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
                         const double2 v0 = __ldg(A.cand + (uint32_t)cur[c]);
                         kv[c] = v0.x;
                         id_v[c] = __double2loint(v0.y);
@@ -432,8 +436,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 if (A.rank_hist) atomicAdd(&A.rank_hist[cur[c]], 1ull);
                 n_acc++;
             } else if (acc[c]) {
-                const int2 ev = kOrdered ? make_int2(id_u[c], id_v[c])
-                                          : make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
+                const int2 ev = kGather == 2 ? make_int2(id_u[c], cur[c])  // (row id, candidate rank)
+                                : kOrdered  ? make_int2(id_u[c], id_v[c])
+                                            : make_int2(min(id_u[c], id_v[c]), max(id_u[c], id_v[c]));
                 if (cnt[c] < cap[c]) {
                     eb[c][cnt[c]] = ev;
                     if (kModel == FM_ECM) A.weights[(eb[c] - A.edges) + cnt[c]] = w[c];
@@ -489,6 +494,7 @@ __global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, const TaskMap
 // by one coalesced pass, then each warp copies 32 of the tasks (slot, then spill part),
 // 4 elements per lane in flight.  Overflowed tasks are skipped (re-run into the final array).
 constexpr int kCopyThreads = 256;
+template <bool kMap>
 __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const TaskMap tm,
                                                           const int64_t *__restrict__ counts,
                                                           const int64_t *__restrict__ dest,
@@ -496,8 +502,15 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
                                                           const int2 *__restrict__ se, const int32_t *__restrict__ sw,
                                                           const int2 *__restrict__ spe, const int32_t *__restrict__ spw,
                                                           int2 *__restrict__ oe, int32_t *__restrict__ ow,
-                                                          int64_t out_cap)
+                                                          int64_t out_cap, const int32_t *__restrict__ rank_map,
+                                                          int ordered)
 {
+    // rank_map: the scratch holds (row id, candidate rank): map the rank to its id and orient
+    auto fin = [&](int2 v) -> int2 {
+        if (!kMap) return v;
+        const int32_t id = __ldg(rank_map + v.y);
+        return ordered ? make_int2(v.x, id) : make_int2(min(v.x, id), max(v.x, id));
+    };
     __shared__ int64_t s_src[kCopyThreads], s_dst[kCopyThreads], s_sp[kCopyThreads];
     __shared__ int32_t s_cnt[kCopyThreads], s_cap[kCopyThreads];
     const int64_t t0 = (int64_t)blockIdx.x * kCopyThreads;
@@ -536,12 +549,22 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const int32_t i = i0 + j * 32 + lane;
-                if (i < n1) v[j] = se[src + i];
+                if (i < n1) v[j] = kMap ? __ldcs(se + src + i) : se[src + i];  // (map: keep L2 for rank_map)
+            }
+            if (kMap) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int32_t i = i0 + j * 32 + lane;
+                    if (i < n1) v[j] = fin(v[j]);
+                }
             }
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 const int32_t i = i0 + j * 32 + lane;
-                if (i < n1) oe[dst + i] = v[j];
+                if (i < n1) {
+                    if (kMap) __stcs(oe + dst + i, v[j]);
+                    else oe[dst + i] = v[j];
+                }
             }
             if (ow) {
                 int32_t x[4];
@@ -558,7 +581,7 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
             }
         }
         for (int32_t i = cap + lane; i < cnt; i += 32) {  // spilled tail
-            oe[dst + i] = spe[sp + i - cap];
+            oe[dst + i] = fin(spe[sp + i - cap]);
             if (ow) ow[dst + i] = spw[sp + i - cap];
         }
     }
@@ -636,10 +659,10 @@ cudaError_t ensure_log_table(cudaStream_t st)
 
 // one instantiation per (model, statistics mode, ECM bound refresh, UBCM gather record, output
 // orientation); kMinB = 3 blocks per SM
-template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, bool kCand, bool kOrdered>
+template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
-    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kCand, kOrdered>;
+    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kGather, kOrdered>;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -672,14 +695,14 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
     return cudaGetLastError();
 }
 
-template <int kModel, bool kStats, bool kRefresh, bool kCand>
+template <int kModel, bool kStats, bool kRefresh, int kGather>
 static cudaError_t launch_sample_o(const SampleArgs &a, cudaStream_t st)
 {
     constexpr int kMinB = kModel == FM_ECM ? FM_SAMPLE_MINB_ECM : FM_SAMPLE_MINB_UBCM;
     // statistics mode writes no pairs: its orientation is irrelevant
     if constexpr (!kStats)
-        if (a.ordered) return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kCand, true>(a, st);
-    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kCand, false>(a, st);
+        if (kGather != 2 && a.ordered) return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, true>(a, st);
+    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, false>(a, st);
 }
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
@@ -696,14 +719,15 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
     // one chain per thread, 3 blocks of 256 per SM (kC = 2, 2 or 4 blocks per SM measured slower)
     const bool stats = a.deg_row != nullptr || a.rank_hist != nullptr;
     if (model == FM_UBCM) {
-        if (a.cand) return stats ? launch_sample_o<FM_UBCM, true, false, true>(a, st)
-                                 : launch_sample_o<FM_UBCM, false, false, true>(a, st);
-        return stats ? launch_sample_o<FM_UBCM, true, false, false>(a, st)
-                     : launch_sample_o<FM_UBCM, false, false, false>(a, st);
+        if (a.rank_out && !stats && !a.rerun_base) return launch_sample_o<FM_UBCM, false, false, 2>(a, st);
+        if (a.cand) return stats ? launch_sample_o<FM_UBCM, true, false, 1>(a, st)
+                                 : launch_sample_o<FM_UBCM, false, false, 1>(a, st);
+        return stats ? launch_sample_o<FM_UBCM, true, false, 0>(a, st)
+                     : launch_sample_o<FM_UBCM, false, false, 0>(a, st);
     }
-    if (stats) return launch_sample_o<FM_ECM, true, false, false>(a, st);
-    return a.ymax_c ? launch_sample_o<FM_ECM, false, true, false>(a, st)
-                    : launch_sample_o<FM_ECM, false, false, false>(a, st);
+    if (stats) return launch_sample_o<FM_ECM, true, false, 0>(a, st);
+    return a.ymax_c ? launch_sample_o<FM_ECM, false, true, 0>(a, st)
+                    : launch_sample_o<FM_ECM, false, false, 0>(a, st);
 }
 
 cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *spill_off,
@@ -718,12 +742,18 @@ cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *c
 
 cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
-                           const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w, cudaStream_t st)
+                           const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w,
+                           const int32_t *rank_map, int ordered, cudaStream_t st)
 {
     if (n_tasks <= 0 || out_cap <= 0) return cudaSuccess;
     count_launch();
-    k_compact<<<(unsigned)((n_tasks + kCopyThreads - 1) / kCopyThreads), kCopyThreads, 0, st>>>(
-        n_tasks, tm, counts, dest, spill_off, scratch_e, scratch_w, spill_e, spill_w, out_e, out_w, out_cap);
+    const unsigned grid = (unsigned)((n_tasks + kCopyThreads - 1) / kCopyThreads);
+    if (rank_map)
+        k_compact<true><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e, scratch_w,
+                                                       spill_e, spill_w, out_e, out_w, out_cap, rank_map, ordered);
+    else
+        k_compact<false><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e, scratch_w,
+                                                        spill_e, spill_w, out_e, out_w, out_cap, rank_map, ordered);
     return cudaGetLastError();
 }
 
