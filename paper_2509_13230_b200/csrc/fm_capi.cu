@@ -422,6 +422,7 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     const int64_t lane_draws[2] = {std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128)),
                                    std::max<int64_t>(1, env_i64("FM_CHUNK_FINE_DRAWS", 64))};
     const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
+    p->slots_aligned = true;
     p->cap_per_sample = 0;
     for (int k = 0; k < 2; k++) {
         const int64_t target = lane_draws[k] * kUnit;
@@ -438,12 +439,14 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
         CK(tmp.get(&work3, cb), "alloc scan tmp");
         CK(scan_exclusive_i64(p->chunk_cap[k], p->chunk_cap[k], nch, work3, cb, st), "scan chunk caps");
         // sum over chunks of floor(1.25 w_c / 2^G) + 16 <= floor(1.25 total / 2^G) + 16 n_chunks
-        int64_t cps = ((total + total / 4) >> kG) + 16 * nch + 16;
+        // sum over chunks of (floor(1.25 w_c / 2^G) + 16 rounded up to 4) <= floor(1.25 total / 2^G) + 19 n_chunks
+        int64_t cps = ((((total + total / 4) >> kG) + 20 * nch + 16) + 3) & ~int64_t(3);
         if (cap_override > 0) {
             count_launch();
             k_fill_caps<<<grid_for(nch + 1, 256), 256, 0, st>>>(p->chunk_cap[k], nch, cap_override);
             CK(cudaGetLastError(), "k_fill_caps");
             cps = cap_override * nch;
+            p->slots_aligned = cap_override % 4 == 0;
         }
         p->cap_per_sample = std::max(p->cap_per_sample, cps);
     }
@@ -584,6 +587,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.cand = p->cand;
         a.ymax_c = (model == FM_ECM && (flags & FM_SAMPLE_BETA_REFRESH)) ? p->ymax : nullptr;
         a.ordered = p->kind != FM_UNDIRECTED;
+        a.buf4 = p->slots_aligned && env_i64("FM_SCRATCH_BUF4", 1) != 0;
         // UBCM with a large candidate set (the kappa array no longer L2-resident): the sampler
         // gathers kappa only and the compaction maps candidate ranks to ids (sampler kernel
         // -14 %, compaction +0.55 ms on config 4: a net gain; at N <= 1e6 the compaction's extra

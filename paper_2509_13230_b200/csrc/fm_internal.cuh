@@ -66,6 +66,7 @@ struct Plan {
     int64_t chunk_target[2]; // work per lane-chunk (units 2^G)
     int64_t wmax;         // bound of one segment's work (units 2^G)
     int64_t cap_per_sample;  // scratch edges per sample (upper bound of chunk_cap[n_chunks])
+    bool slots_aligned;      // every scratch slot starts at a multiple of 4 edges (32 bytes)
     unsigned int *dev_flags; // planner invariant flags (checked by fm_sample_*)
 };
 

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) k_chunks(int64_t n_seg, int64_t n_chunks,
     chunk_seg[c] = g0;
     if (c == n_chunks - 1) chunk_seg[n_chunks] = n_seg;
     const int64_t w = work_pre[g1] - work_pre[g0];
-    chunk_cap[c] = ((w + (w >> 2)) >> kG) + 16;
+    chunk_cap[c] = ((((w + (w >> 2)) >> kG) + 16) + 3) & ~int64_t(3);  // whole 32-byte sectors of edges
 }
 
 // the sampler's per-candidate gather record (Plan::cand)
