@@ -15,6 +15,11 @@
 #include "fm_internal.cuh"
 #include "fm_plan_kernels.cuh"
 
+#ifdef FM_TRACE
+namespace fm {
+void dump_trace();  // fm_sample.cu (timeline instrumentation build)
+}
+#endif
 namespace fm {
 std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches += n; }
@@ -509,6 +514,7 @@ static TaskMap make_task_map(const Plan *p, int64_t n_samples, int64_t *n_tasks)
     return tm;
 }
 
+
 static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
                              uint32_t flags, void *cuda_stream, fm_edges *out)
 {
@@ -657,6 +663,9 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
            "read plan flags");
         tw.end(st);
         CK(cudaStreamSynchronize(st), "sync (sample)");
+#ifdef FM_TRACE
+        fm::dump_trace();
+#endif
         if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
         const int64_t total = offsets_h[n_samples];
         if (total > out_cap) {  // (pathological overflow) redo the write into an exact-size list

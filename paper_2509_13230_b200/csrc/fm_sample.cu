@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -29,6 +30,24 @@
 namespace fm {
 
 __device__ LogTable g_logtab;
+#ifdef FM_TRACE
+// per-warp timeline of the last sampler launch (instrumentation build, scripts/trace_run.py):
+// start, first time the task queue was exhausted for the warp, end (globaltimer ns), iterations,
+// iterations after exhaustion, SM id
+__device__ unsigned long long g_trace[4096][6];
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+#endif
 
 namespace {
 
@@ -217,7 +236,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         return U01(ws);
     };
 
+#ifdef FM_TRACE
+    const unsigned long long tr_t0 = gtimer();
+    unsigned long long tr_done = 0, tr_it = 0, tr_it_done = 0;
+#endif
     for (;;) {
+#ifdef FM_TRACE
+        tr_it++;
+        if (warp_done) {
+            tr_it_done++;
+            if (!tr_done) tr_done = gtimer();
+        }
+#endif
         // ---- 1. task management (only when a chain of the warp has no segment left; a single
         //      vote otherwise): such chains take the next task ids of the warp's batch (the next
         //      batch is requested as soon as one is opened) ----
@@ -483,6 +513,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             }
         }
     }
+#ifdef FM_TRACE
+    if (lane == 0 && !A.rerun_base) {
+        const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        if (wi < 4096) {
+            g_trace[wi][0] = tr_t0;
+            g_trace[wi][1] = tr_done;
+            g_trace[wi][2] = gtimer();
+            g_trace[wi][3] = tr_it;
+            g_trace[wi][4] = tr_it_done;
+            g_trace[wi][5] = smid();
+        }
+    }
+#endif
     if (A.rerun_base) return;
     const unsigned dr = __reduce_add_sync(0xffffffffu, n_draw);
     const unsigned ac = __reduce_add_sync(0xffffffffu, n_acc);
@@ -666,6 +709,22 @@ std::mutex g_tab_mu;
 bool g_tab_done[64] = {false};
 
 }  // namespace
+
+#ifdef FM_TRACE
+void dump_trace()
+{
+    static unsigned long long h[4096][6];
+    if (cudaMemcpyFromSymbol(h, g_trace, sizeof(h)) != cudaSuccess) return;
+    const char *path = getenv("FM_TRACE_FILE");
+    FILE *f = fopen(path ? path : "/tmp/fm_trace.bin", "wb");
+    if (f) {
+        fwrite(h, sizeof(h), 1, f);
+        fclose(f);
+    }
+    static unsigned long long z[4096][6];
+    cudaMemcpyToSymbol(g_trace, z, sizeof(z));
+}
+#endif
 
 cudaError_t ensure_log_table(cudaStream_t st)
 {
