@@ -1,9 +1,9 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab16_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab16_pytest.log
-( FM_LIB_VARIANT=trace timeout 120 python scripts/trace_run.py 2 100
-  FM_LIB_VARIANT=trace timeout 120 python scripts/trace_run.py 3 100
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab17_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab17_pytest.log
+( FM_LIB_VARIANT=trace timeout 120 python scripts/trace_run.py 2 100 | head -6
+  FM_LIB_VARIANT=trace timeout 120 python scripts/trace_run.py 3 100 | head -6
   FM_LIB_VARIANT=prev timeout 120 python scripts/probe_tail.py 2
   timeout 120 python scripts/probe_tail.py 2
-  FM_TAIL_FACTOR=1 timeout 120 python scripts/probe_tail.py 2
-  FM_TAIL_FACTOR=0 timeout 120 python scripts/probe_tail.py 2 ) 2>&1 | tee gpurun_out/ab16.txt
-AB_RUNS=$'prev;FM_LIB_VARIANT=prev;--config 2\nbase;;--config 2\nprev3;FM_LIB_VARIANT=prev;--config 3\nbase3;;--config 3\nprev4;FM_LIB_VARIANT=prev;--config 4\nbase4;;--config 4\nprev5;FM_LIB_VARIANT=prev;--config 5\nbase5;;--config 5' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee -a gpurun_out/ab16.txt
+  FM_TAIL_FACTOR=0 timeout 120 python scripts/probe_tail.py 2
+  FM_HEAVY_DRAWS=32 timeout 120 python scripts/probe_tail.py 2 ) 2>&1 | tee gpurun_out/ab17.txt
+AB_RUNS=$'prev;FM_LIB_VARIANT=prev;--config 2\nbase;;--config 2\nprev3;FM_LIB_VARIANT=prev;--config 3\nbase3;;--config 3\nprev4;FM_LIB_VARIANT=prev;--config 4\nbase4;;--config 4\nprev5;FM_LIB_VARIANT=prev;--config 5\nbase5;;--config 5' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee -a gpurun_out/ab17.txt
