@@ -394,7 +394,7 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     // row_m now holds row_seg (exclusive prefix of the per-row segment counts, n+1 entries)
     int64_t *seg_work;
     CK(tmp.get(&seg_work, n_seg + 1), "alloc seg_work");
-    CK(cudaMallocAsync((void **)&p->rec, sizeof(SegRec) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
+    CK(cudaMallocAsync((void **)&p->rec, (size_t)kRecStride(model) * std::max<int64_t>(n_seg, 1), st), "alloc rec");
     if (n_seg > 0) {
         // segment -> row map for large plans: exclusive scan of the row-start flags (small plans:
         // a per-block search in k_emit, two launches fewer)
@@ -887,8 +887,14 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
     if (ymax && p->ymax) CK(cudaMemcpy(ymax, p->ymax, ((size_t)p->nc + 1) * 8, cudaMemcpyDeviceToHost), "ymax");
     if (ly_s && p->ly_s) CK(cudaMemcpy(ly_s, p->ly_s, n * 8, cudaMemcpyDeviceToHost), "ly_s");
     if (s && (seg || seg_h0 || seg_x0 || seg_d0 || seg_omT || seg_iomT)) {  // from the packed records
+        const size_t stride = (size_t)kRecStride(p->model);
+        std::vector<unsigned char> raw(s * stride);
+        CK(cudaMemcpy(raw.data(), p->rec, s * stride, cudaMemcpyDeviceToHost), "seg records");
         std::vector<SegRec> r(s);
-        CK(cudaMemcpy(r.data(), p->rec, s * sizeof(SegRec), cudaMemcpyDeviceToHost), "seg records");
+        for (size_t g = 0; g < s; g++) {
+            memset(&r[g], 0, sizeof(SegRec));
+            memcpy(&r[g], raw.data() + g * stride, stride);
+        }
         for (size_t g = 0; g < s; g++) {
             if (seg) {
                 seg[4 * g] = r[g].u;

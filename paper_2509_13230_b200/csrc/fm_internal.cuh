@@ -21,7 +21,9 @@ enum : uint32_t {
     kFlagWeightSat = 8u,  // ECM weight clamped
 };
 
-// one plan segment as the sampler reads it (96 B in 16-byte parts; UBCM reads the first 64 B)
+// one plan segment as the sampler reads it (96 B in 16-byte parts).  The plan stores UBCM records
+// with a 64-byte stride (the first four parts; the ECM fields are not stored)
+__host__ __device__ constexpr int kRecStride(int model) { return model == 0 ? 64 : 96; }
 struct __align__(16) SegRec {
     int32_t u, a, b, sigma;  // focal rank, candidates [a, b), segment index in the row
     double h0, x0;           // initial bound at a-1: q0 = x0 / d0, h0 = -log(1 - q0)
@@ -56,7 +58,7 @@ struct Plan {
     // a4 segments
     int64_t n_seg;
     double *ly_s;       // [n] ECM: log y_s
-    SegRec *rec;        // [n_seg] packed copy of the above for the sampler
+    unsigned char *rec; // [n_seg] packed records for the sampler, stride kRecStride(model) bytes
     int64_t est_draws;  // sum of segment work estimates / 2^G
     // chunking (does not change results)
     // two chunkings: [0] coarse (most samples), [1] fine (the last samples of a call: short tail)

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, in
                                               const double *__restrict__ ymax, const uint64_t *__restrict__ P,
                                               PlanScalars *sc, const RowInfo *__restrict__ rows,
                                               const int64_t *__restrict__ row_seg,
-                                              const int64_t *__restrict__ seg_row_x, SegRec *__restrict__ rec,
+                                              const int64_t *__restrict__ seg_row_x, unsigned char *__restrict__ rec,
                                               int64_t *__restrict__ seg_work)
 {
     __shared__ __align__(16) SegRec s_rec[256];  // the block's records, written out coalesced
@@ -291,10 +291,12 @@ __global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, in
     }
     __syncthreads();
     // 16-byte words of the block's records, consecutive threads -> consecutive addresses
+    // (the record stride is kRecStride(model): UBCM stores the first 4 of the 6 parts)
     const int4 *src = reinterpret_cast<const int4 *>(s_rec);
-    int4 *dst = reinterpret_cast<int4 *>(rec + g0);
+    const int words = kRecStride(model) / 16;
+    int4 *dst = reinterpret_cast<int4 *>(rec + g0 * kRecStride(model));
     constexpr int kWords = (int)(sizeof(SegRec) / 16);
-    for (int i = threadIdx.x; i < nb * kWords; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < nb * words; i += blockDim.x) dst[i] = src[(i / words) * kWords + i % words];
 }
 
 // row-start flags for k_emit's segment -> row map: flag[row_seg[u]] = 1 for rows with segments

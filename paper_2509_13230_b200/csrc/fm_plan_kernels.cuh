@@ -45,7 +45,7 @@ __global__ void k_rows(int model, int kind, int64_t n, int64_t nc, int64_t S, co
 __global__ void k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg, const double *kappa_s,
                        const double *y_s, const double *ly_s, const int32_t *perm, const int32_t *excl,
                        const double *ckappa, const double *ymax, const uint64_t *P, PlanScalars *sc,
-                       const RowInfo *rows, const int64_t *row_seg, const int64_t *seg_row_x, SegRec *rec,
+                       const RowInfo *rows, const int64_t *row_seg, const int64_t *seg_row_x, unsigned char *rec,
                        int64_t *seg_work);
 __global__ void k_row_starts(int64_t n, const int64_t *row_seg, int64_t *flag);
 __global__ void k_rank_of(int64_t nc, const int32_t *cperm, int32_t *crank);
@@ -100,7 +100,7 @@ __device__ __forceinline__ void task_decode(const TaskMap &M, int64_t t, int64_t
 }
 
 struct SampleArgs {
-    const SegRec *rec;
+    const unsigned char *rec;      // segment records, stride kRecStride(model)
     const double *kappa_s, *y_s, *ly_s;  // CANDIDATE arrays (the - set; the rows themselves if undirected)
     const int32_t *perm;                 // candidate rank -> id
     const double2 *cand;                 // packed gather records (Plan::cand)

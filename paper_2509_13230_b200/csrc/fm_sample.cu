@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 asm("ld.shared.v2.f64 {%0,%1}, [%2+%3];" : "=d"(p5.x), "=d"(p5.y) : "r"(sa), "n"(5 * kPart));
             }
         } else {
-            const SegRec *r = A.rec + g[c];
+            const SegRec *r = reinterpret_cast<const SegRec *>(A.rec + (size_t)g[c] * kRecStride(kModel));
             p0 = *reinterpret_cast<const int4 *>(r);
             p1 = *reinterpret_cast<const double2 *>(&r->h0);
             p2 = *reinterpret_cast<const double2 *>(&r->d0);
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         g[c]++;
         act[c] = true;
         if (g[c] < g_end[c]) {
-            const char *src = reinterpret_cast<const char *>(A.rec + g[c]);
+            const unsigned char *src = A.rec + (size_t)g[c] * kRecStride(kModel);
             constexpr int parts = kModel == FM_ECM ? 6 : 4;
 #pragma unroll
             for (int k = 0; k < parts; k++)

@@ -1,9 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab17_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab17_pytest.log
-( FM_LIB_VARIANT=trace timeout 120 python scripts/trace_run.py 2 100 | head -6
-  FM_LIB_VARIANT=trace timeout 120 python scripts/trace_run.py 3 100 | head -6
-  FM_LIB_VARIANT=prev timeout 120 python scripts/probe_tail.py 2
-  timeout 120 python scripts/probe_tail.py 2
-  FM_TAIL_FACTOR=0 timeout 120 python scripts/probe_tail.py 2
-  FM_HEAVY_DRAWS=32 timeout 120 python scripts/probe_tail.py 2 ) 2>&1 | tee gpurun_out/ab17.txt
-AB_RUNS=$'prev;FM_LIB_VARIANT=prev;--config 2\nbase;;--config 2\nprev3;FM_LIB_VARIANT=prev;--config 3\nbase3;;--config 3\nprev4;FM_LIB_VARIANT=prev;--config 4\nbase4;;--config 4\nprev5;FM_LIB_VARIANT=prev;--config 5\nbase5;;--config 5' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee -a gpurun_out/ab17.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_bipartite.py tests/test_gpu_degrees.py -x -q > gpurun_out/ab19_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab19_pytest.log
+AB_RUNS=$'prev;FM_LIB_VARIANT=prev;--config 2\nrec64;;--config 2\ns12;FM_LIB_VARIANT=s12;--config 2\nprev4;FM_LIB_VARIANT=prev;--config 4\nrec64_4;;--config 4\ns12_4;FM_LIB_VARIANT=s12;--config 4\nprev5;FM_LIB_VARIANT=prev;--config 5\nrec64_5;;--config 5' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee gpurun_out/ab19.txt
