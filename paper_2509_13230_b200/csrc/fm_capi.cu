@@ -894,6 +894,7 @@ fm_status fm_plan_export(const fm_plan *plan, int32_t *perm, double *kappa_s, do
         for (size_t g = 0; g < s; g++) {
             memset(&r[g], 0, sizeof(SegRec));
             memcpy(&r[g], raw.data() + g * stride, stride);
+            if (p->model == FM_UBCM) r[g].omT = r[g].iomT = 1.0;  // (not stored: UBCM's bound has T = 0)
         }
         for (size_t g = 0; g < s; g++) {
             if (seg) {
