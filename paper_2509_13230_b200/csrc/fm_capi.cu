@@ -638,11 +638,12 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                 e = cudaMallocAsync(&own->weights, sizeof(int32_t) * std::max<int64_t>(cap, 1), st);
             return e;
         };
-        auto write_out = [&](int64_t cap) -> cudaError_t {
-            cudaError_t e = launch_compact(cap, n_tasks, tm, counts, dest, spill_off, se, sw, a.spill_e, a.spill_w,
-                                           (int2 *)own->edges, (int32_t *)own->weights,
-                                           a.rank_out ? p->cperm : nullptr, a.ordered, st);
-            if (e != cudaSuccess) return e;
+        auto write_out = [&](int64_t cap, bool compact, bool rerun) -> cudaError_t {
+            cudaError_t e = compact ? launch_compact(cap, n_tasks, tm, counts, dest, spill_off, se, sw, a.spill_e,
+                                                     a.spill_w, (int2 *)own->edges, (int32_t *)own->weights,
+                                                     a.rank_out ? p->cperm : nullptr, a.ordered, st)
+                                    : cudaSuccess;
+            if (e != cudaSuccess || !rerun) return e;
             SampleArgs r = a;  // deterministic re-run of overflowed tasks straight into the final list
             r.n_tasks = n_tasks;
             r.n_tasks_dev = &hd->n_overflow;
@@ -653,8 +654,9 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             r.weights = (int32_t *)own->weights;
             return launch_sample(model, r, st);
         };
+        // the re-run of overflowed tasks (rare) is launched only after the synchronisation shows one
         CK(alloc_out(out_cap), "alloc edges");
-        CK(write_out(out_cap), "compact / rerun");
+        CK(write_out(out_cap, true, false), "compact");
         CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
            "read offsets");
         CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
@@ -674,8 +676,11 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             own->edges = own->weights = nullptr;
             out_cap = total;
             CK(alloc_out(out_cap), "alloc edges");
-            CK(write_out(out_cap), "compact / rerun");
+            CK(write_out(out_cap, true, h.n_overflow > 0), "compact / rerun");
             CK(cudaStreamSynchronize(st), "sync (sample, exact)");
+        } else if (h.n_overflow > 0) {
+            CK(write_out(out_cap, false, true), "rerun");
+            CK(cudaStreamSynchronize(st), "sync (sample, rerun)");
         }
         out->n_edges = total;
     }

@@ -430,13 +430,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     }
                 } else {
                     const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ord, 0.0))) : 1.0;
-                    const double t = __dmul_rn(yu[c], yv[c]);  // (ECM: yv defined on every path, see above)
+                    // (yv + 0*us), like kv: the gathered y is used only after the Philox rounds (the
+                    // plain product was scheduled first and stalled every warp on the gather:
+                    // 20 % of the ECM kernel's stall samples)
+                    const double t = __dmul_rn(yu[c], __dadd_rn(yv[c], __dmul_rn(ord, 0.0)));
                     const double Dp = __dadd_rn(__dsub_rn(1.0, t), z);
                     // the bound for the candidates still ahead: per segment 1 - T = omT, or (kRefresh,
                     // R17) per reached candidate 1 - y_u Ymax[cur+1]
                     double omb = omT[c], iomb = iomT[c];
                     if (kRefresh && landed[c]) {
-                        omb = __dsub_rn(1.0, __dmul_rn(yu[c], ymn[c]));
+                        omb = __dsub_rn(1.0, __dmul_rn(yu[c], __dadd_rn(ymn[c], __dmul_rn(ord, 0.0))));  // (ordered too)
                         iomb = __drcp_rn(omb);
                     }
                     const double hn = fm_log1p(__dmul_rn(z, iomb), T);

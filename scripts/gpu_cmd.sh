@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ab20_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab20_pytest.log
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ab22_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab22_pytest.log
+AB_RUNS=$'prev3;FM_LIB_VARIANT=prev;--config 3\nbase3;;--config 3\nprevr;FM_LIB_VARIANT=prev;--config 3 --refresh\nbaser;;--config 3 --refresh\nprev2;FM_LIB_VARIANT=prev;--config 2\nbase2;;--config 2' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee gpurun_out/ab22.txt
