@@ -122,11 +122,12 @@ def test_batch_equals_singles_and_determinism():
                                   np.sort(E[e.offsets[s]:e.offsets[s + 1]].view(np.int64).ravel()))
 
 
-def test_scratch_overflow_rerun_is_identical(monkeypatch):
+@pytest.mark.parametrize("cap", ["7", "8"])  # 8: 32-byte-aligned slots (whole-sector writes) that still overflow
+def test_scratch_overflow_rerun_is_identical(monkeypatch, cap):
     x, y = WL.random_fitness(6, 20_000, 2.3, 0.02, ecm=True)
     for yy in (None, y):
         _, e, E, W = gpu_run(x, yy, 64, 5, 3)
-        monkeypatch.setenv("FM_DEBUG_SCRATCH_CAP", "7")
+        monkeypatch.setenv("FM_DEBUG_SCRATCH_CAP", cap)
         _, e2, E2, W2 = gpu_run(x, yy, 64, 5, 3)
         monkeypatch.delenv("FM_DEBUG_SCRATCH_CAP")
         assert e2.flags & fm.FM_FLAG_SCRATCH_RERUN
@@ -135,6 +136,24 @@ def test_scratch_overflow_rerun_is_identical(monkeypatch):
         for s in range(3):
             a, b = e.offsets[s], e.offsets[s + 1]
             assert np.array_equal(key(E[a:b]), key(E2[a:b]))
+
+
+@pytest.mark.parametrize("env", [{"FM_UBCM_RANK_OUT_MIN": "0"},   # kappa-only gathers, ranks mapped by the compaction
+                                 {"FM_UBCM_CAND_MIN": "0"},       # one 16-byte (kappa, id) record per candidate
+                                 {"FM_SCRATCH_BUF4": "0"}])       # one 8-byte store per edge
+def test_ubcm_gather_and_store_modes_identical(O, monkeypatch, env):
+    """The sampler's alternative gather / store paths produce the default path's edge list byte for
+    byte (and the oracle's on the small case)."""
+    x, _ = WL.random_fitness(11, 30_011, 2.5, 0.02)
+    _, e, E, _ = gpu_run(x, None, 64, 9, 4)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, e2, E2, _ = gpu_run(x, None, 64, 9, 4)
+    assert np.array_equal(e.offsets, e2.offsets) and np.array_equal(E, E2)
+    xs, _ = WL.random_fitness(12, 3001, 2.5, 0.05)
+    check_parity(O, xs, None, 16, seed=3, n_samples=3, exact=True)
+    for k in env:
+        monkeypatch.delenv(k)
 
 
 def test_edge_cases(O):
