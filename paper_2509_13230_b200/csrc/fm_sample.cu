@@ -412,11 +412,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 // next draw, log1p of this candidate) stay independent; exact since us in (0,1)
                 // (kv is read only if landed: the ?: evaluates the selected operand only)
                 const double Enew = -fm_log(us, T);
-#ifdef FM_ELOG_FIRST
-                const double ord = Enew;  // the gathered kv is used after E of the next draw
-#else
-                const double ord = us;
-#endif
+                const double ord = us;  // (ordering after E of the next draw instead measured no faster)
                 if (kModel == FM_UBCM) {
                     const double X = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ord, 0.0))) : 1.0;
                     const double D = __dadd_rn(1.0, X);

@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab25_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab25_pytest.log
-AB_RUNS=$'prev;FM_LIB_VARIANT=prev;--config 2\nbase;;--config 2\nprev3;FM_LIB_VARIANT=prev;--config 3\nbase3;;--config 3\nprev4;FM_LIB_VARIANT=prev;--config 4\nbase4;;--config 4\nprev5;FM_LIB_VARIANT=prev;--config 5\nbase5;;--config 5' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee gpurun_out/ab25.txt
+ncu --set full --clock-control none --import-source on -k regex:k_sample -s 2 -c 1 -o gpurun_out/ab26_ecm python bench.py --config 3 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu rc=$?"
