@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         uint32_t w_land[kC], w_wt[kC];
         double kv[kC], yv[kC], lyv[kC], ymn[kC];
         int32_t id_v[kC];
+        double idd[kC];  // the record word holding the id (low half), see the ECM block below
 #pragma unroll
         for (int c = 0; c < kC; c++) {
             landed[c] = false;
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
             if (kModel == FM_ECM) {
                 kv[c] = yv[c] = lyv[c] = 0.0;
                 id_v[c] = 0;
+                idd[c] = 0.0;
                 ymn[c] = 0.0;
             }
             if (act[c] && !fresh[c]) {
@@ -376,14 +378,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         kv[c] = v0.x;
                         yv[c] = v0.y;
                         lyv[c] = v1.x;
-                        id_v[c] = __double2loint(v1.y);
+                        idd[c] = v1.y;
                         if (kRefresh) ymn[c] = __ldg(A.ymax_c + cur[c] + 1);
                     } else if (kGather == 2) {  // UBCM: κ only, the id is mapped in the compaction
                         kv[c] = A.kappa_s[cur[c]];
                     } else if (kGather == 1) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
                         const double2 v0 = __ldg(A.cand + (uint32_t)cur[c]);
                         kv[c] = v0.x;
-                        id_v[c] = __double2loint(v0.y);
+                        idd[c] = v0.y;
                     } else {  // UBCM, L2-resident arrays: two plain gathers (measured no slower)
                         kv[c] = A.kappa_s[cur[c]];
                         id_v[c] = A.perm[cur[c]];
@@ -425,7 +427,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         rh[c] = __drcp_rn(hn);
                     }
                 } else {
-                    const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ord, 0.0))) : 1.0;
+                    // (us + hid) * 0: hid = the record's unused high id word (zero) as a double, "read"
+                    // here where the gather is awaited anyway -- left dead, its register was reused
+                    // right after the gather and the write-after-write wait on the in-flight load
+                    // stalled every warp before Philox (15 % of the ECM kernel's stall samples)
+                    const double hid = __hiloint2double(__double2hiint(idd[c]), 0);
+                    const double z = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(__dadd_rn(ord, hid), 0.0)))
+                                               : 1.0;
                     // (yv + 0*us), like kv: the gathered y is used only after the Philox rounds (the
                     // plain product was scheduled first and stalled every warp on the gather:
                     // 20 % of the ECM kernel's stall samples)
@@ -463,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         // ---- 6. append accepted edges to the tasks' slots, in draw order ----
 #pragma unroll
         for (int c = 0; c < kC; c++) {
+            if (kModel == FM_ECM || kGather == 1) id_v[c] = __double2loint(idd[c]);
             if (kStats && acc[c]) {  // statistics mode (NEXT-3): degrees/strengths, no edge list
                 if (A.deg_row) {
                     row_acc[c]++;
