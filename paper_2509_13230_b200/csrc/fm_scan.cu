@@ -165,12 +165,26 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64
     const int64_t base = tile * kTile + (int64_t)threadIdx.x * kItems;
     uint64_t v[kItems];
     uint64_t acc = 0;
+    // a thread's 8 items are 64 contiguous bytes: 16-byte vector loads when the 8 are in range and
+    // the array is 16-byte aligned (every caller's is)
+    const bool vec = base + kItems <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (vec) {
+        const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(in + base);
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
-        const int64_t i = base + k;
-        v[k] = i < n ? in[i] : 0;
-        acc += v[k];
+        for (int k = 0; k < kItems / 2; k++) {
+            const ulonglong2 w = q[k];
+            v[2 * k] = w.x;
+            v[2 * k + 1] = w.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kItems; k++) {
+            const int64_t i = base + k;
+            v[k] = i < n ? in[i] : 0;
+        }
     }
+#pragma unroll
+    for (int k = 0; k < kItems; k++) acc += v[k];
     uint64_t tot;
     const uint64_t exc = block_exclusive<SumU64>(acc, &tot);
     if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
@@ -202,11 +216,22 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64
     }
     __syncthreads();
     uint64_t pre = s_prefix + exc;
+    if (vec) {
+        ulonglong2 *q = reinterpret_cast<ulonglong2 *>(out + base);
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
-        const int64_t i = base + k;
-        if (i < n) out[i] = pre;
-        pre += v[k];
+        for (int k = 0; k < kItems / 2; k++) {
+            const uint64_t a0 = pre;
+            pre += v[2 * k];
+            q[k] = make_ulonglong2(a0, pre);
+            pre += v[2 * k + 1];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kItems; k++) {
+            const int64_t i = base + k;
+            if (i < n) out[i] = pre;
+            pre += v[k];
+        }
     }
     if (tile == (n - 1) / kTile && threadIdx.x == ((n - 1) % kTile) / kItems) out[n] = pre;  // total
 }
