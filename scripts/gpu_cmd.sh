@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-AB_RUNS=$'base4;;--config 4\ncs4;FM_LIB_VARIANT=cs4;--config 4' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee gpurun_out/ab33.txt
+ncu --set full --clock-control none --import-source on -k regex:k_pass -s 3 -c 1 -o gpurun_out/kpass4 python bench.py --config 4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu rc=$?"
