@@ -347,9 +347,10 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
         CK(cudaGetLastError(), "k_excl");
     }
 
-    // packed gather records: ECM always; UBCM when kappa + perm (12 B per candidate) would not stay
-    // resident in L2 (FM_UBCM_CAND_MIN candidates, default 2^21: 24 MB)
-    const bool want_cand = model == FM_ECM || n2 >= env_i64("FM_UBCM_CAND_MIN", int64_t(1) << 21);
+    // packed gather records: ECM always (32 B); UBCM one 16-byte (kappa, id) record per candidate at
+    // every size (config 2 sampler -3 %, config 5 -4 % against two arrays, once the record's dead
+    // word no longer stalled the gather; FM_UBCM_CAND_MIN raises the threshold for A/B runs)
+    const bool want_cand = model == FM_ECM || n2 >= env_i64("FM_UBCM_CAND_MIN", 0);
     if (want_cand)
         CK(cudaMallocAsync((void **)&p->cand, sizeof(double2) * kCandWords(model) * std::max<int64_t>(n2, 1), st),
            "alloc cand");

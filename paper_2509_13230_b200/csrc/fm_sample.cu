@@ -416,7 +416,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 const double Enew = -fm_log(us, T);
                 const double ord = us;  // (ordering after E of the next draw instead measured no faster)
                 if (kModel == FM_UBCM) {
-                    const double X = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ord, 0.0))) : 1.0;
+                    double ordu = ord;
+                    if (kGather == 1)  // the record's unused high id word read here (see the ECM block)
+                        ordu = __dadd_rn(ord, __hiloint2double(__double2hiint(idd[c]), 0));
+                    const double X = landed[c] ? __dmul_rn(ku[c], __dadd_rn(kv[c], __dmul_rn(ordu, 0.0))) : 1.0;
                     const double D = __dadd_rn(1.0, X);
                     const double hn = fm_log1p(X, T);
                     if (landed[c]) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)

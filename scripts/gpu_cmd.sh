@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k regex:k_pass -s 3 -c 1 -o gpurun_out/kpass4 python bench.py --config 4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu rc=$?"
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ab35_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab35_pytest.log
+AB_RUNS=$'base2;;--config 2\nbase4;;--config 4\nbase5;;--config 5' AB_STEPS=5 bash scripts/abx.sh 2>&1 | tee gpurun_out/ab35.txt

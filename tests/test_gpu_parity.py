@@ -139,7 +139,7 @@ def test_scratch_overflow_rerun_is_identical(monkeypatch, cap):
 
 
 @pytest.mark.parametrize("env", [{"FM_UBCM_RANK_OUT_MIN": "0"},   # kappa-only gathers, ranks mapped by the compaction
-                                 {"FM_UBCM_CAND_MIN": "0"},       # one 16-byte (kappa, id) record per candidate
+                                 {"FM_UBCM_CAND_MIN": str(1 << 40)},  # kappa and id from two arrays (no record)
                                  {"FM_SCRATCH_BUF4": "0"}])       # one 8-byte store per edge
 def test_ubcm_gather_and_store_modes_identical(O, monkeypatch, env):
     """The sampler's alternative gather / store paths produce the default path's edge list byte for
