@@ -571,8 +571,12 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         Hdr *hd;
         const int64_t slots = n_samples * p->cap_per_sample;
         const int64_t spill_cap = slots / 32 + 65536;
-        CK(tmp.get(&se, slots + spill_cap), "alloc scratch edges");
-        if (model == FM_ECM) CK(tmp.get(&sw, slots + spill_cap), "alloc scratch weights");
+        // ECM with aligned slots: 16-byte (src, dst, w, 0) records in the slots (two int2 words per
+        // edge); the spill area keeps separate edge / weight arrays
+        const bool ecm_rec = model == FM_ECM && p->slots_aligned && env_i64("FM_SCRATCH_BUF4", 1) != 0;
+        const int64_t slot_words = ecm_rec ? 2 * slots : slots, wslots = ecm_rec ? 0 : slots;
+        CK(tmp.get(&se, slot_words + spill_cap), "alloc scratch edges");
+        if (model == FM_ECM) CK(tmp.get(&sw, wslots + spill_cap), "alloc scratch weights");
         CK(tmp.get(&spill_off, n_tasks), "alloc spill offsets");
         CK(tmp.get(&counts, n_tasks + 1), "alloc counts");
         CK(tmp.get(&dest, n_tasks + 1), "alloc dest");
@@ -610,8 +614,8 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.edges = se;
         a.weights = sw;
         a.counts = counts;
-        a.spill_e = se + slots;
-        a.spill_w = sw ? sw + slots : nullptr;
+        a.spill_e = se + slot_words;
+        a.spill_w = sw ? sw + wslots : nullptr;
         a.spill_counter = &hd->spill_counter;
         a.spill_cap = spill_cap;
         a.spill_off = spill_off;
@@ -642,7 +646,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         auto write_out = [&](int64_t cap, bool compact, bool rerun) -> cudaError_t {
             cudaError_t e = compact ? launch_compact(cap, n_tasks, tm, counts, dest, spill_off, se, sw, a.spill_e,
                                                      a.spill_w, (int2 *)own->edges, (int32_t *)own->weights,
-                                                     a.rank_out ? p->cperm : nullptr, a.ordered, st)
+                                                     a.rank_out ? p->cperm : nullptr, a.ordered, ecm_rec ? 1 : 0, st)
                                     : cudaSuccess;
             if (e != cudaSuccess || !rerun) return e;
             SampleArgs r = a;  // deterministic re-run of overflowed tasks straight into the final list

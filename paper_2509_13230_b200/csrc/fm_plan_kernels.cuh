@@ -143,7 +143,7 @@ cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *c
 cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w,
-                           const int32_t *rank_map, int ordered, cudaStream_t st);
+                           const int32_t *rank_map, int ordered, int ecm_rec, cudaStream_t st);
 cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets, cudaStream_t st);
 // out[i] += in[i], i < n (uint64)
 cudaError_t launch_add_u64(const uint64_t *in, uint64_t *out, int64_t n, cudaStream_t st);

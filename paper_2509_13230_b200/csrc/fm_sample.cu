@@ -108,8 +108,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // UBCM: the last < 4 accepted edges of each lane's slot, so that the slot is written in whole
     // 32-byte sectors (structure of arrays: conflict-free)
     __shared__ int2 s_eb[kModel == FM_UBCM ? 4 : 1][kThreads];
-    // (UBCM only: the ECM kernel, at its register limit, measured 4 % slower with it)
     const bool buf4 = kModel == FM_UBCM && A.buf4 && !A.rerun_base && !kStats;
+    // ECM: the scratch holds one 16-byte (src, dst, w, 0) record per edge, written two per sector
+    // (the lane's previous record waits in shared memory); the compaction splits the records into
+    // the edge and weight arrays (separate 8- and 4-byte stores wrote two partial sectors per edge)
+    __shared__ int4 s_er[kModel == FM_ECM ? kThreads : 1];
+    const bool aos = kModel == FM_ECM && A.buf4 && !A.rerun_base && !kStats;
     const SmemLogTab T{A.lc, load_logtab()};
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
@@ -271,6 +275,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         for (int j = 0; j < (n1 & 3); j++) {
                             eb[c][(n1 & ~3) + j] = s_eb[j][threadIdx.x];
                         }
+                    }
+                    if (aos) {
+                        const int32_t n1 = min(cnt[c], cap[c]);
+                        if (n1 & 1) reinterpret_cast<int4 *>(A.edges)[(eb[c] - A.edges) + n1 - 1] = s_er[threadIdx.x];
                     }
                     if (!A.rerun_base && !kStats) {
                         A.counts[tk] = cnt[c];
@@ -508,6 +516,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                                 q[1] = make_int4(e2.x, e2.y, ev.x, ev.y);
                             }
                         }
+                    } else if (aos) {
+                        const int4 rec = make_int4(ev.x, ev.y, w[c], 0);
+                        if ((cnt[c] & 1) == 0) {
+                            s_er[threadIdx.x] = rec;
+                        } else {  // records cnt-1, cnt: one sector
+                            int4 *q = reinterpret_cast<int4 *>(A.edges) + ((eb[c] - A.edges) + cnt[c] - 1);
+                            q[0] = s_er[threadIdx.x];
+                            q[1] = rec;
+                        }
                     } else {
                         eb[c][cnt[c]] = ev;
                         if (kModel == FM_ECM) A.weights[(eb[c] - A.edges) + cnt[c]] = w[c];
@@ -577,7 +594,7 @@ __global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, const TaskMap
 // by one coalesced pass, then each warp copies 32 of the tasks (slot, then spill part),
 // 4 elements per lane in flight.  Overflowed tasks are skipped (re-run into the final array).
 constexpr int kCopyThreads = 256;
-template <bool kMap>
+template <bool kMap, bool kRec>
 __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const TaskMap tm,
                                                           const int64_t *__restrict__ counts,
                                                           const int64_t *__restrict__ dest,
@@ -627,7 +644,26 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
         if (cnt == 0) continue;
         const int64_t src = s_src[k], dst = s_dst[k], sp = s_sp[k];
         const int32_t n1 = min(cnt, cap);
-        for (int32_t i0 = 0; i0 < n1; i0 += 128) {
+        if (kRec) {  // ECM 16-byte records (src, dst, w, 0) -> edge and weight arrays
+            const int4 *sr = reinterpret_cast<const int4 *>(se);
+            for (int32_t i0 = 0; i0 < n1; i0 += 128) {
+                int4 v[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int32_t i = i0 + j * 32 + lane;
+                    if (i < n1) v[j] = sr[src + i];
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int32_t i = i0 + j * 32 + lane;
+                    if (i < n1) {
+                        oe[dst + i] = make_int2(v[j].x, v[j].y);
+                        ow[dst + i] = v[j].z;
+                    }
+                }
+            }
+        }
+        for (int32_t i0 = 0; i0 < (kRec ? 0 : n1); i0 += 128) {
             int2 v[4];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -842,17 +878,23 @@ cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *c
 cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w,
-                           const int32_t *rank_map, int ordered, cudaStream_t st)
+                           const int32_t *rank_map, int ordered, int ecm_rec, cudaStream_t st)
 {
     if (n_tasks <= 0 || out_cap <= 0) return cudaSuccess;
     count_launch();
     const unsigned grid = (unsigned)((n_tasks + kCopyThreads - 1) / kCopyThreads);
     if (rank_map)
-        k_compact<true><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e, scratch_w,
-                                                       spill_e, spill_w, out_e, out_w, out_cap, rank_map, ordered);
+        k_compact<true, false><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e,
+                                                              scratch_w, spill_e, spill_w, out_e, out_w, out_cap,
+                                                              rank_map, ordered);
+    else if (ecm_rec)
+        k_compact<false, true><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e,
+                                                              scratch_w, spill_e, spill_w, out_e, out_w, out_cap,
+                                                              rank_map, ordered);
     else
-        k_compact<false><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e, scratch_w,
-                                                        spill_e, spill_w, out_e, out_w, out_cap, rank_map, ordered);
+        k_compact<false, false><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e,
+                                                               scratch_w, spill_e, spill_w, out_e, out_w, out_cap,
+                                                               rank_map, ordered);
     return cudaGetLastError();
 }
 
