@@ -594,6 +594,10 @@ __global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, const TaskMap
 // by one coalesced pass, then each warp copies 32 of the tasks (slot, then spill part),
 // 4 elements per lane in flight.  Overflowed tasks are skipped (re-run into the final array).
 constexpr int kCopyThreads = 256;
+#ifndef FM_COPY_UNROLL
+#define FM_COPY_UNROLL 4
+#endif
+constexpr int kCU = FM_COPY_UNROLL;  // elements per lane in flight
 template <bool kMap, bool kRec>
 __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const TaskMap tm,
                                                           const int64_t *__restrict__ counts,
@@ -646,15 +650,15 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
         const int32_t n1 = min(cnt, cap);
         if (kRec) {  // ECM 16-byte records (src, dst, w, 0) -> edge and weight arrays
             const int4 *sr = reinterpret_cast<const int4 *>(se);
-            for (int32_t i0 = 0; i0 < n1; i0 += 128) {
-                int4 v[4];
+            for (int32_t i0 = 0; i0 < n1; i0 += 32 * kCU) {
+                int4 v[kCU];
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
+                for (int j = 0; j < kCU; j++) {
                     const int32_t i = i0 + j * 32 + lane;
                     if (i < n1) v[j] = sr[src + i];
                 }
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
+                for (int j = 0; j < kCU; j++) {
                     const int32_t i = i0 + j * 32 + lane;
                     if (i < n1) {
                         oe[dst + i] = make_int2(v[j].x, v[j].y);
@@ -663,22 +667,22 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
                 }
             }
         }
-        for (int32_t i0 = 0; i0 < (kRec ? 0 : n1); i0 += 128) {
-            int2 v[4];
+        for (int32_t i0 = 0; i0 < (kRec ? 0 : n1); i0 += 32 * kCU) {
+            int2 v[kCU];
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
+            for (int j = 0; j < kCU; j++) {
                 const int32_t i = i0 + j * 32 + lane;
                 if (i < n1) v[j] = kMap ? __ldcs(se + src + i) : se[src + i];  // (map: keep L2 for rank_map)
             }
             if (kMap) {
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
+                for (int j = 0; j < kCU; j++) {
                     const int32_t i = i0 + j * 32 + lane;
                     if (i < n1) v[j] = fin(v[j]);
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
+            for (int j = 0; j < kCU; j++) {
                 const int32_t i = i0 + j * 32 + lane;
                 if (i < n1) {
                     if (kMap) __stcs(oe + dst + i, v[j]);
@@ -686,14 +690,14 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
                 }
             }
             if (ow) {
-                int32_t x[4];
+                int32_t x[kCU];
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
+                for (int j = 0; j < kCU; j++) {
                     const int32_t i = i0 + j * 32 + lane;
                     if (i < n1) x[j] = sw[src + i];
                 }
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
+                for (int j = 0; j < kCU; j++) {
                     const int32_t i = i0 + j * 32 + lane;
                     if (i < n1) ow[dst + i] = x[j];
                 }
