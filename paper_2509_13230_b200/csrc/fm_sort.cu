@@ -68,12 +68,18 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     uint64_t key[kItems];
     int32_t val[kItems];
     int dig[kItems], loc[kItems];
+    // all of the thread's loads issued before the first rank (the warp syncs below would
+    // otherwise serialise one load latency per item)
 #pragma unroll
     for (int r = 0; r < kItems; r++) {
         const int64_t i = wbase + r * 32 + lane;  // warp-contiguous, in input order
         const bool ok = i < n;
-        key[r] = ok ? kin[i] : 0;
-        val[r] = ok ? vin[i] : 0;
+        key[r] = ok ? __ldcs(kin + i) : 0;
+        val[r] = ok ? __ldcs(vin + i) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kItems; r++) {
+        const bool ok = wbase + r * 32 + lane < n;
         dig[r] = ok ? (int)((key[r] >> shift) & 0xFF) : kRadix;
         const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
         const int rank = __popc(peers & lt);
