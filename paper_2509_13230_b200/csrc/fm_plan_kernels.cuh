@@ -113,6 +113,9 @@ struct SampleArgs {
     const int64_t *task_list;      // NULL: task = queue index; else task_list[queue index]
     int ordered;                   // bipartite / directed: emit (row id, candidate id) as is (R16)
     int rank_out;                  // UBCM: scratch pairs hold (row id, candidate rank), mapped by k_compact
+    int64_t il_s[2];               // > 0: queue order chunk-major within each chunking's samples (il_s[k]
+                                   // samples each), so the samples of one lane-chunk run together and
+                                   // share its segment records in L2; 0: sample-major (queue = task)
     int buf4;                      // scratch slots 32-byte aligned: edges are written 4 at a time (whole sectors)
     unsigned long long *task_counter;  // global queue head (zeroed before each launch)
     int2 *edges;                   // scratch (normal) or final array (rerun)

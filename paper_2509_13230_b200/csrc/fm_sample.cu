@@ -303,7 +303,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
                 }
                 if (needc && !warp_done && my < n_tasks) {
-                    const int64_t t = A.task_list ? A.task_list[my] : my;
+                    int64_t t = A.task_list ? A.task_list[my] : my;
+                    if (A.il_s[0] > 0 && !A.task_list) {  // chunk-major queue -> canonical task index
+                        const int kq = my < A.tm.t_split ? 0 : 1;
+                        const int64_t m = kq ? my - A.tm.t_split : my, ns = A.il_s[kq];
+                        const int64_t cq = m / ns;
+                        t = (kq ? A.tm.t_split : 0) + (m - cq * ns) * A.tm.n_chunks[kq] + cq;
+                    }
                     int64_t s, ch;
                     int kk;
                     task_decode(A.tm, t, s, ch, kk);

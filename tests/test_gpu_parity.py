@@ -156,6 +156,27 @@ def test_ubcm_gather_and_store_modes_identical(O, monkeypatch, env):
         monkeypatch.delenv(k)
 
 
+@pytest.mark.parametrize("ecm", [False, True])
+def test_chunk_major_queue_identical(O, monkeypatch, ecm):
+    """The chunk-major task queue (the samples of one lane-chunk back to back, on by default at
+    N >= 2^19) only reorders work: the edge list equals the sample-major queue's byte for byte,
+    and the oracle's on the small case."""
+    x, y = WL.random_fitness(13, 40_009, 2.4, 0.02, ecm=True)
+    yy = y if ecm else None
+    res = []
+    for v in ("0", str(1 << 40)):  # forced on / forced off
+        monkeypatch.setenv("FM_INTERLEAVE_MIN", v)
+        _, e, E, W = gpu_run(x, yy, 64, 21, 5)
+        res.append((e.offsets, E, W))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    if ecm:
+        assert np.array_equal(res[0][2], res[1][2])
+    monkeypatch.setenv("FM_INTERLEAVE_MIN", "0")
+    xs, ys = WL.random_fitness(14, 3001, 2.5, 0.05, ecm=True)
+    check_parity(O, xs, ys if ecm else None, 16, seed=4, n_samples=3, exact=True)
+    monkeypatch.delenv("FM_INTERLEAVE_MIN")
+
+
 def test_edge_cases(O):
     # complete graph, empty graph, N = 2, zero samples
     n = 300
