@@ -60,6 +60,9 @@ namespace {
 #ifndef FM_SAMPLE_MINB_ECM
 #define FM_SAMPLE_MINB_ECM 3
 #endif
+#ifndef FM_SAMPLE_MINB_RANKOUT  // UBCM rank-out path (N >= 2^21: DRAM-latency-bound gathers)
+#define FM_SAMPLE_MINB_RANKOUT 3
+#endif
 constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
 constexpr int kBatch = 64;  // tasks per warp batch
 
@@ -843,7 +846,8 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 template <int kModel, bool kStats, bool kRefresh, int kGather>
 static cudaError_t launch_sample_o(const SampleArgs &a, cudaStream_t st)
 {
-    constexpr int kMinB = kModel == FM_ECM ? FM_SAMPLE_MINB_ECM : FM_SAMPLE_MINB_UBCM;
+    constexpr int kMinB = kModel == FM_ECM ? FM_SAMPLE_MINB_ECM
+                          : kGather == 2   ? FM_SAMPLE_MINB_RANKOUT : FM_SAMPLE_MINB_UBCM;
     // statistics mode writes no pairs: its orientation is irrelevant
     if constexpr (!kStats)
         if (kGather != 2 && a.ordered) return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, true>(a, st);
