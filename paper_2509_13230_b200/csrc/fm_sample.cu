@@ -61,7 +61,7 @@ namespace {
 #define FM_SAMPLE_MINB_ECM 3
 #endif
 #ifndef FM_SAMPLE_MINB_RANKOUT  // UBCM rank-out path (N >= 2^21: DRAM-latency-bound gathers)
-#define FM_SAMPLE_MINB_RANKOUT 3
+#define FM_SAMPLE_MINB_RANKOUT 4
 #endif
 constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
 constexpr int kBatch = 64;  // tasks per warp batch
