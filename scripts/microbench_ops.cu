@@ -61,24 +61,37 @@ __global__ void k_log(double *out, uint32_t seed)
     for (int i = 0; i < M; i++) acc = __dadd_rn(acc, log(u01(hsh(i + seed, t))));
     out[t] = acc;
 }
-// log1p over the sampler's range of X = kappa_u kappa_v (1e-9 .. 1e3): X = u01 * 2^(e), e in [-30, 10]
+// log1p over the sampler's range of X = kappa_u kappa_v (1e-9 .. 1e3): X = u01 * 2^e with the
+// exponent e in [-30, 10] WARP-UNIFORM (a function of the warp index and the iteration only), so
+// every warp call takes one range path of log1p: the divergent cost of a warp whose lanes take
+// both paths is not counted as algorithmic work (round-2 fix: the round-1 kernels drew e per lane
+// from (h >> 26) - 30, i.e. e in [-30, 33], and executed both paths in most warps).
+// emin/erange select a sub-range: [-30, 10] (all), [-30, -2] (the small-X path), [0, 10] (large X).
+template <int emin, int erange>
+__device__ __forceinline__ int warp_exp(uint32_t i)
+{
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    return emin + (int)((hsh(i * 7u + 3u, w) >> 8) % (uint32_t)erange);
+}
+template <int emin, int erange>
 __global__ void k_base_log1p(double *out, uint32_t seed)
 {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     double acc = 0;
     for (int i = 0; i < M; i++) {
         const uint32_t h = hsh(i + seed, t);
-        acc = __dadd_rn(acc, ldexp(u01(h), (int)(h >> 26) - 30 + 0));
+        acc = __dadd_rn(acc, ldexp(u01(h), warp_exp<emin, erange>(i + seed)));
     }
     out[t] = acc;
 }
+template <int emin, int erange>
 __global__ void k_log1p(double *out, uint32_t seed)
 {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     double acc = 0;
     for (int i = 0; i < M; i++) {
         const uint32_t h = hsh(i + seed, t);
-        acc = __dadd_rn(acc, log1p(ldexp(u01(h), (int)(h >> 26) - 30 + 0)));
+        acc = __dadd_rn(acc, log1p(ldexp(u01(h), warp_exp<emin, erange>(i + seed))));
     }
     out[t] = acc;
 }
@@ -145,8 +158,8 @@ int main()
     printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"threads\": %lld, \"iters\": %d, \"kernels\": {", sms, clk, nthreads,
            M);
     const char *names[] = {"base", "base_u01", "philox", "log", "base_log1p", "log1p", "base_ddiv", "ddiv", "dfma8",
-                           "int8"};
-    for (int k = 0; k < 10; k++) {
+                           "int8", "base_log1p_small", "log1p_small", "base_log1p_large", "log1p_large"};
+    for (int k = 0; k < 14; k++) {
         float best = 1e30f;
         for (int rep = 0; rep < 5; rep++) {
             cudaEventRecord(a);
@@ -155,12 +168,16 @@ int main()
             case 1: k_base_u01<<<blocks, threads>>>(out, rep); break;
             case 2: k_philox<<<blocks, threads>>>(out, rep, 0x12345678u, 0x9abcdef0u); break;
             case 3: k_log<<<blocks, threads>>>(out, rep); break;
-            case 4: k_base_log1p<<<blocks, threads>>>(out, rep); break;
-            case 5: k_log1p<<<blocks, threads>>>(out, rep); break;
+            case 4: k_base_log1p<-30, 41><<<blocks, threads>>>(out, rep); break;
+            case 5: k_log1p<-30, 41><<<blocks, threads>>>(out, rep); break;
             case 6: k_base_ddiv<<<blocks, threads>>>(out, rep); break;
             case 7: k_ddiv<<<blocks, threads>>>(out, rep); break;
             case 8: k_dfma<<<blocks, threads>>>(out, rep); break;
             case 9: k_int<<<blocks, threads>>>(out, rep); break;
+            case 10: k_base_log1p<-30, 29><<<blocks, threads>>>(out, rep); break;
+            case 11: k_log1p<-30, 29><<<blocks, threads>>>(out, rep); break;
+            case 12: k_base_log1p<0, 11><<<blocks, threads>>>(out, rep); break;
+            case 13: k_log1p<0, 11><<<blocks, threads>>>(out, rep); break;
             }
             cudaEventRecord(b);
             cudaEventSynchronize(b);

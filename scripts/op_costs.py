@@ -25,7 +25,8 @@ def load(path):
             continue
         if hdr and len(r) == len(hdr):
             d = dict(zip(hdr, r))
-            name = d["Kernel Name"].split("(")[0].split("<")[0]
+            # template args kept: "void k_log1p<(int)-30, 41>(double *, ...)" -> k_log1p<-30,41>
+            name = d["Kernel Name"].replace("void ", "").replace("(int)", "").split("(")[0].replace(" ", "")
             data.setdefault(name, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     return data
 
@@ -43,9 +44,13 @@ def main():
     warp_calls = round(warp_calls / M) * M
     per_call = lambda k, base, key: (d[k][key] - d[base][key]) / warp_calls  # noqa: E731
     ops = {}
+    # log1p: warp-uniform exponent e in [-30, 10] (each warp call takes one range path; round 2),
+    # and per path: e in [-30, -2] (small X) and e in [0, 10] (large X)
     for op, k, base in (("philox", "k_philox", "k_base"), ("log", "k_log", "k_base_u01"),
-                        ("log1p", "k_log1p", "k_base_log1p"), ("ddiv", "k_ddiv", "k_base_ddiv"),
-                        ("u01", "k_base_u01", "k_base")):
+                        ("log1p", "k_log1p<-30,41>", "k_base_log1p<-30,41>"), ("ddiv", "k_ddiv", "k_base_ddiv"),
+                        ("u01", "k_base_u01", "k_base"),
+                        ("log1p_small_path", "k_log1p<-30,29>", "k_base_log1p<-30,29>"),
+                        ("log1p_large_path", "k_log1p<0,11>", "k_base_log1p<0,11>")):
         ops[op] = {"inst": per_call(k, base, "sm__inst_executed.sum"),
                    "fp64": per_call(k, base, "sm__inst_executed_pipe_fp64.sum")}
     ops["ddiv"]["inst"] += 1.0  # the base kernel has a DMUL in place of the division
@@ -89,7 +94,8 @@ def main():
                      "ecm": {"draw": draw_e, "landed": land_e, "accepted": acc_e}},
         "notes": "inst/fp64 = warp-instructions per warp-level unit (32 lanes). Peaks: issue 4/clk/SM "
                  "(4 SMSPs x 1), FP64 pipe 2/clk/SM (64 lanes; measured DFMA rate alongside), "
-                 "at the 1965 MHz max SM clock.",
+                 "at the 1965 MHz max SM clock. log1p: warp-uniform input exponent in [-30, 10] (one range "
+                 "path per warp call; divergence not counted as algorithmic work); per-path costs alongside.",
     }
     json.dump(out, sys.stdout, indent=1)
     print()
