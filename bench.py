@@ -2,13 +2,16 @@
 """Benchmark of the sampler hot path (BASELINE.json metric: accepted edges/s and proposals/s on
 one B200, and % of the sampler roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl own|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl own|reference]
 
 One STEP = one pass of the whole hot path over one batch:
 fm_sort_plan(x) + fm_sample_ubcm/ecm(plan, seed, R samples) + release, inputs resident in HBM.
-Default workload: BASELINE.json configs[1] (config 2: UBCM, N=1e5, gamma 2.5, mean degree 20,
-R = 100 samples per call).  Each rank samples its own R samples (sample indices rank*R ...):
-weak scaling, no data-path collective (the samples are independent).
+Default workload: BASELINE.json configs[4] (config 5: UBCM ensemble batch, N=1e6, gamma 2.3,
+mean degree 50, R = 64 samples per call, ~1.6e9 edges = 12.8 GB of int32 pairs per step), the
+largest configuration that fits one GPU's call; configs 1-4 via --config.  Each rank samples its
+own R samples (sample indices rank*R ...): weak scaling, no data-path collective (the samples are
+independent).  `--gpus N` without a torchrun environment re-launches itself
+under torch.distributed.run with N ranks (one per GPU).
 
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the launching
 stream, with a 256 MiB L2 flush (a write larger than the 126 MB L2) between steps outside the
@@ -47,7 +50,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--seg-target", type=int, default=256)
     ap.add_argument("--impl", choices=["own", "reference"], default="own")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -56,7 +59,45 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--refresh", action="store_true",
                     help="ECM: per-candidate beta_min refresh (fm_sample_ecm_ex FM_SAMPLE_BETA_REFRESH, NEXT-4)")
+    ap.add_argument("--selftest-dist", action="store_true",
+                    help="CPU self-test of the rank logic (gloo, no GPU, no sampling): shards and reductions")
     return ap.parse_args()
+
+
+def self_launch(args) -> bool:
+    """`--gpus N` (N > 1) outside torchrun: re-run this command under torch.distributed.run with N
+    ranks on this node (127.0.0.1 rendezvous).  Returns True if it did (the caller then exits)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc != 0:
+        raise SystemExit(rc)
+    return True
+
+
+def run_selftest_dist(args):
+    """The multi-rank plumbing of the own arm without a GPU (gloo): each rank takes its sample shard
+    and a synthetic per-rank time and count; rank 0 prints the reduced values as one JSON line."""
+    import torch.distributed as dist
+    rank, _, world = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    R = WL.workload(args.config).n_samples
+    first, n = D.shard_samples(rank, world, R)
+    t_max = D.reduce_max(10.0 + rank)
+    shards = D.reduce_sum([first if r == rank else 0 for r in range(world)])
+    edges = D.reduce_sum([1000 * (rank + 1)])[0]
+    if rank == 0:
+        print(json.dumps({"selftest": "dist", "n_gpus": world, "samples_per_rank": n, "first_samples": shards,
+                          "t_max": t_max, "edges_all": edges}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 dist_env = D.env_rank_world
@@ -116,7 +157,8 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ roofline
-def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: int = 2, refresh: bool = False):
+def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: int = 2, refresh: bool = False,
+             call_ms: float | None = None):
     """Roofline of the dominant kernel k_sample.
 
     Compute term: algorithmic warp-instructions of the chain (op list of DESIGN 7.1, per-op
@@ -153,17 +195,31 @@ def roofline(model: str, counters: dict, kernel_ms: float, launches: int, cfg: i
         ach, peak, unit = fp64_l / t / 1e9, fp64_peak / 1e9, "G fp64 warp-inst/s"
     else:
         ach, peak, unit = inst_l / t / 1e9, issue_peak / 1e9, "G warp-inst/s"
-    traffic = None
+    traffic = traffic_compact = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    tag = f"{model}_cfg{cfg}" + ("_refresh" if refresh else "")
     if os.path.exists(tpath):
-        tr = json.load(open(tpath)).get("k_sample", {}).get(f"{model}_cfg{cfg}" + ("_refresh" if refresh else ""))
+        tj = json.load(open(tpath))
+        tr = tj.get("k_sample", {}).get(tag)
         if tr:
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+        tc = tj.get("k_compact", {}).get(tag)
+        if tc:
+            traffic_compact = tc["dram_read_bytes"] + tc["dram_write_bytes"]
+    t_roof = max(t_issue, t_fp64, t_mem)
+    # the whole fm_sample_* call (sampler + count scan + offsets + compaction), SURVEY 8(d) timing
+    call = None
+    if call_ms is not None:
+        tc_l = call_ms * 1e-3 / max(1, launches)
+        call = {"ms_per_call": tc_l * 1e3, "frac": t_roof / tc_l,
+                "note": "t_roof of the call's algorithmic work / (k_sample + write phase) device time per call"}
     return {"bound": "alu" if bound != "hbm" else "hbm", "resource": bound, "achieved": ach, "peak": peak,
-            "unit": unit, "frac": ach / peak, "traffic": traffic,
-            "traffic_note": "dram read+write bytes per launch from one ncu --set full capture (profiles/traffic.json)",
+            "unit": unit, "frac": ach / peak, "traffic": traffic, "traffic_compact": traffic_compact,
+            "traffic_note": "dram read+write bytes per launch of k_sample (traffic) and k_compact (traffic_compact) "
+                            "from ncu --set full captures (profiles/traffic.json)",
+            "call": call,
             "kernel": "k_sample",
-            "kernel_ms_per_launch": t * 1e3, "t_roof_ms": max(t_issue, t_fp64, t_mem) * 1e3,
+            "kernel_ms_per_launch": t * 1e3, "t_roof_ms": t_roof * 1e3,
             "terms_ms": {"issue": t_issue * 1e3, "fp64": t_fp64 * 1e3, "hbm": t_mem * 1e3},
             "alg_warp_inst_per_launch": inst_l, "alg_fp64_warp_inst_per_launch": fp64_l,
             "alg_bytes_per_launch": bytes_l, "peak_source": f"op_costs.json (measured) + hbm {hbm_src}",
@@ -313,21 +369,25 @@ def run_own(args):
         eh = torch.empty((cap, 2), dtype=torch.int32).pin_memory()
         wh = torch.empty(cap, dtype=torch.int32).pin_memory() if y is not None else None
         e_ms, e_edges, h2d, d2h = [], 0, 0, 0
+        e_phase = {"plan_sample": 0.0, "d2h": 0.0}
         for k in range(args.e2e_steps + 1):
             flush.fill_(k & 0xFF)
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a, m, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             a.record()
             plan = fm.sort_plan(xh, yh, seg_target=args.seg_target)       # host pointers -> H2D inside
             e = sample(plan, w.seed, n_samples=R, first_sample=first)
             if e.n_edges > eh.shape[0]:
                 eh = torch.empty((e.n_edges, 2), dtype=torch.int32).pin_memory()
                 wh = torch.empty(e.n_edges, dtype=torch.int32).pin_memory() if y is not None else None
+            m.record()
             e.to_host(eh, wh)                                                 # D2H of the result
             b.record()
             b.synchronize()
             if k > 0:  # first iteration is a warm-up
                 e_ms.append(a.elapsed_time(b))
+                e_phase["plan_sample"] += a.elapsed_time(m) / args.e2e_steps
+                e_phase["d2h"] += m.elapsed_time(b) / args.e2e_steps
                 e_edges += e.n_edges
                 h2d = x.nbytes + (0 if y is None else y.nbytes)
                 d2h = e.n_edges * (8 if y is None else 12) + 8 * (R + 1)
@@ -335,7 +395,8 @@ def run_own(args):
             plan.free()
         e2e = {"value": e_edges / (sum(e_ms) * 1e-3), "unit": "edges/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(e_ms), "steps": len(e_ms),
-               "host_buffers": "pinned"}
+               "host_buffers": "pinned", "phase_ms": e_phase,
+               "d2h_gbs": d2h / (e_phase["d2h"] * 1e-3) / 1e9 if e_phase["d2h"] > 0 else None}
 
     if rank != 0:
         if world > 1:
@@ -343,7 +404,8 @@ def run_own(args):
         return
 
     refresh = args.refresh and w.model == "ecm"
-    rf = roofline(w.model, tot, tim["sample_ms"], max(1, tim["sample_launches"]), cfg=args.config, refresh=refresh)
+    rf = roofline(w.model, tot, tim["sample_ms"], max(1, tim["sample_launches"]), cfg=args.config, refresh=refresh,
+                  call_ms=tim["sample_ms"] + tim["write_ms"])
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         c = cpu_oracle_run(w, x, y, args.seg_target, args.cpu_seconds, refresh=refresh)
@@ -369,7 +431,11 @@ def run_own(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if self_launch(args):
+        return
+    if args.selftest_dist:
+        run_selftest_dist(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_own(args)

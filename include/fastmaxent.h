@@ -14,6 +14,9 @@
  * Conventions for every entry point:
  *  - Returns an fm_status; never aborts.  On error nothing is allocated, *out is zeroed, and
  *    fm_last_error() returns a thread-local message.
+ *  - Device temporaries come from the device's default stream-ordered memory pool, whose release
+ *    threshold the library bounds at the first call on a device (FM_POOL_RELEASE_BYTES, default
+ *    1/4 of the device memory): freed memory above it is returned to the device.
  *  - All work is ordered on the caller's CUDA stream `cuda_stream` (cudaStream_t; NULL = the
  *    legacy default stream) on the current device.
  *  - Input pointers may be HOST or DEVICE memory (detected with cudaPointerGetAttributes); they
@@ -40,7 +43,11 @@ typedef enum {
                             sample range beyond 2^32 */
     FM_ERR_NOMEM = -2,   /* device or host allocation failed */
     FM_ERR_CUDA = -3,    /* CUDA runtime error (no device, launch failure, ...) */
-    FM_ERR_BOUND = -4,   /* contract violation p > q (1 + 2^-50) detected (debug checks) */
+    FM_ERR_BOUND = -4,   /* contract violation p > q (1 + 2^-50) at a landed candidate ("abort,
+                            never clamp"; R13).  Checked only when the environment has
+                            FM_DEBUG_CHECKS=1 at call time; the call then releases everything and
+                            fills nothing.  (FM_DEBUG_BAD_BOUND=1 at fm_sort_plan time is a test
+                            hook that builds a plan with too-small initial bounds.) */
     FM_ERR_STATE = -5    /* wrong object / model mismatch / internal invariant violated */
 } fm_status;
 
@@ -157,6 +164,20 @@ fm_status fm_sample_degrees(const fm_plan *plan, uint64_t seed, int64_t first_sa
  * Integer atomics: deterministic.  Synchronises the stream once. */
 fm_status fm_sample_richclub(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples,
                              void *cuda_stream, uint64_t *e_top, fm_counters *out);
+
+/* Closed-form expectations under the model (the targets of the statistical gates):
+ * for each listed node i (nodes: int32[n_nodes] node ids, HOST or DEVICE; NULL = all n nodes, in
+ * order), over every j != i,
+ *     k[c] = sum_j p_ij,  kvar[c] = sum_j p_ij (1 - p_ij)             (Eq. 4)
+ *     s[c] = sum_j p_ij / (1 - t_ij),  svar[c] = sum_j Var[w_ij]      (ECM only; Eq. 3-5)
+ * i.e. the expected degree / strength of node i and their variances (independent pairs, P:L90-93;
+ * E[w_ij] = p/(1-t), E[w_ij^2] = p(1+t)/(1-t)^2).  p in fitness form as for the sampler (x, y as in
+ * fm_sort_plan, HOST or DEVICE float64[n]).  O(n * n_nodes) fp64 pair evaluations with compensated
+ * summation.  Outputs: caller-owned DEVICE float64[n_nodes]; any may be NULL (s/svar must be NULL
+ * for the UBCM).  Synchronises the stream. */
+fm_status fm_expected_degrees(fm_model model, int64_t n, const double *x, const double *y, const int32_t *nodes,
+                              int64_t n_nodes, double *k, double *kvar, double *s, double *svar,
+                              void *cuda_stream);
 
 /* Copy a result to caller-owned HOST buffers: edges_host int32[2*n_edges], weights_host
  * int32[n_edges] (may be NULL).  Stream-ordered; synchronises the stream. */

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfastmaxent.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["fm_scan.cu", "fm_sort.cu", "fm_plan.cu", "fm_sample.cu", "fm_capi.cu"]
+SOURCES = ["fm_scan.cu", "fm_sort.cu", "fm_plan.cu", "fm_sample.cu", "fm_expect.cu", "fm_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O2", "-I", INC, "-I", CSRC,

@@ -10,6 +10,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "fm_internal.cuh"
@@ -113,16 +114,28 @@ struct Allocs {
     }
 };
 
-void configure_pool_once(int dev)
+// The stream-ordered temporaries of a call (scratch ~1.3x the edge list) come from the device's
+// default pool.  Its release threshold is bounded (FM_POOL_RELEASE_BYTES, default 1/4 of the
+// device memory): memory freed by a call stays mapped for the next call up to that size (no
+// remapping per call), and anything above it is returned to the device at the next
+// synchronisation, so a large call does not starve other allocators (PyTorch's) afterwards.
+void configure_pool(int dev)
 {
-    static std::once_flag once;
-    std::call_once(once, [dev]() {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    });
+    static std::mutex mu;
+    static bool done[kMaxDevices] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= kMaxDevices || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        size_t total = 0;
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) total = prop.totalGlobalMem;
+        const char *v = getenv("FM_POOL_RELEASE_BYTES");
+        uint64_t thr = v && *v ? strtoull(v, nullptr, 10) : (uint64_t)(total / 4);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
 }
 
 bool is_device_ptr(const void *p)
@@ -282,7 +295,7 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     cudaStream_t st = (cudaStream_t)cuda_stream;
     int dev = 0;
     CK(cudaGetDevice(&dev), "cudaGetDevice");
-    configure_pool_once(dev);
+    configure_pool(dev);
     Allocs tmp(st);
     PhaseTimer timer;
     timer.begin(kPhasePlan, st);
@@ -303,6 +316,7 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     p->nc = n2;
     p->S = seg_target;
     p->device = dev;
+    p->out_ratio = 1.03;
     struct PlanGuard {
         Plan *p;
         ~PlanGuard() { if (p) plan_release(p); }
@@ -388,6 +402,9 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     CK(cudaStreamSynchronize(st), "sync (rows)");
     if (h_sc.flags & kErrInvalid)
         return fail(FM_ERR_INVALID, "invalid fitness: x must be finite >= 0, y in [0,1), kappa_max^4 finite");
+    // the sampler indexes segments with 32-bit integers
+    if (n_seg > INT32_MAX)
+        return fail(FM_ERR_INVALID, "plan has %lld segments (> 2^31-1): raise seg_target", (long long)n_seg);
     p->F = h_sc.F;
     p->n_seg = n_seg;
     p->wmax = h_sc.wmax;
@@ -415,6 +432,13 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
                                                      p->ly_s, p->perm, p->excl, p->ckappa, p->ymax, P, sc, rows,
                                                      row_m, seg_row_x, p->rec, seg_work);
         CK(cudaGetLastError(), "k_emit");
+        // test hook: a plan whose initial bounds are too small (p > q at the first candidates), for
+        // the FM_DEBUG_CHECKS contract check (FM_ERR_BOUND)
+        if (env_i64("FM_DEBUG_BAD_BOUND", 0)) {
+            count_launch();
+            k_debug_scale_bound<<<grid_for(n_seg, 256), 256, 0, st>>>(p->rec, n_seg, kRecStride(model), 1e-3);
+            CK(cudaGetLastError(), "k_debug_scale_bound");
+        }
     }
     {
         const size_t wb = scan_tmp_bytes(n_seg + 1);
@@ -618,7 +642,6 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.tm = tm;
         a.key = philox_key(seed);
         a.lc = log_consts();
-    a.lc = log_consts();
         a.first_sample = (uint32_t)first_sample;
         a.n_tasks = n_tasks;
         a.task_counter = &hd->task_counter;
@@ -632,6 +655,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.spill_off = spill_off;
         a.counters = hd->counters;
         a.flags = &hd->flags;
+        a.check = env_i64("FM_DEBUG_CHECKS", 0) != 0;
         PhaseTimer ts, tw;
         ts.begin(kPhaseSample, st);
         CK(launch_sample(model, a, st), "sampler launch");
@@ -644,10 +668,21 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
         CK(launch_offsets(n_samples, tm, dest, offs_d, st), "offsets");
         CK(launch_overflow(n_tasks, tm, counts, spill_off, &hd->n_overflow, ovl, st), "overflow check");
-        // The final list is allocated up front with the scratch's capacity (an upper bound unless a
-        // task overflowed both its slot and its spill region), so compaction and the re-run of
-        // overflowed tasks are queued without a host round trip; one synchronisation at the end.
+        // The final list is allocated up front (so compaction and the re-run of overflowed tasks are
+        // queued without a host round trip; one synchronisation at the end) with the plan's capacity
+        // hint: out_ratio x (estimated draws - segments) per sample + 8 sigma-like margin, at most the
+        // scratch's capacity.  A call whose edges exceed it redoes the write into an exact-size list.
         int64_t out_cap = slots + spill_cap;
+        {
+            double ratio;
+            {
+                std::lock_guard<std::mutex> lk(g_mu);
+                ratio = p->out_ratio;
+            }
+            const double per = (double)std::max<int64_t>(1, p->est_draws - p->n_seg);
+            const double est = ratio * per * (double)n_samples + 8.0 * std::sqrt(per * (double)n_samples) + 4096.0;
+            if (est < (double)out_cap) out_cap = (int64_t)est;
+        }
         auto alloc_out = [&](int64_t cap) -> cudaError_t {
             cudaError_t e = cudaMallocAsync(&own->edges, sizeof(int2) * std::max<int64_t>(cap, 1), st);
             if (e == cudaSuccess && model == FM_ECM)
@@ -685,7 +720,17 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         fm::dump_trace();
 #endif
         if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
+        // FM_DEBUG_CHECKS: a p > q contract violation fails the call; nothing stays allocated
+        if (h.flags & kErrBound) return fail(FM_ERR_BOUND, "p > q (1 + 2^-50) detected at a landed candidate (S:L289)");
         const int64_t total = offsets_h[n_samples];
+        {  // capacity hint for the next call on this plan
+            const double per = (double)std::max<int64_t>(1, p->est_draws - p->n_seg) * (double)n_samples;
+            const double seen = (double)total / per;
+            std::lock_guard<std::mutex> lk(g_mu);
+            Plan *pm = const_cast<Plan *>(p);
+            if (total > out_cap) pm->out_ratio = std::max(pm->out_ratio, seen * 1.02);
+            else if (n_samples >= 8) pm->out_ratio = std::max(seen * 1.01, 0.05);
+        }
         if (total > out_cap) {  // (pathological overflow) redo the write into an exact-size list
             cudaFreeAsync(own->edges, st);
             if (own->weights) cudaFreeAsync(own->weights, st);
@@ -718,7 +763,6 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         std::lock_guard<std::mutex> lk(g_mu);
         g_owners.insert(own);
     }
-    if (h.flags & kErrBound) return fail(FM_ERR_BOUND, "p > q detected");
     return FM_OK;
 }
 
@@ -816,6 +860,7 @@ static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, 
     a.str_row = (unsigned long long *)str_plus;
     a.str_col = (unsigned long long *)str_minus;
     a.rank_hist = (unsigned long long *)rank_hist;
+    a.check = env_i64("FM_DEBUG_CHECKS", 0) != 0;
     PhaseTimer ts;
     ts.begin(kPhaseSample, st);
     CK(launch_sample(p->model, a, st), "sampler launch (degrees)");
@@ -826,6 +871,7 @@ static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, 
     CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st), "read flags");
     CK(cudaStreamSynchronize(st), "sync (degrees)");
     if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
+    if (h.flags & kErrBound) return fail(FM_ERR_BOUND, "p > q (1 + 2^-50) detected at a landed candidate (S:L289)");
     if (out) {
         out->draws = (int64_t)h.counters[0];
         out->landed = out->draws - p->n_seg * n_samples;  // one terminal draw per segment
@@ -949,6 +995,42 @@ fm_status fm_plan_export_candidates(const fm_plan *plan, int32_t *cperm, double 
         if (p->excl) CK(cudaMemcpy(excl, p->excl, n * 4, cudaMemcpyDeviceToHost), "excl");
         else for (size_t u = 0; u < n; u++) excl[u] = -1;
     }
+    return FM_OK;
+}
+
+fm_status fm_expected_degrees(fm_model model, int64_t n, const double *x, const double *y, const int32_t *nodes,
+                              int64_t n_nodes, double *k, double *kvar, double *s, double *svar, void *cuda_stream)
+{
+    if (model != FM_UBCM && model != FM_ECM) return fail(FM_ERR_INVALID, "unknown model %d", (int)model);
+    if (n < 1 || n > INT32_MAX) return fail(FM_ERR_INVALID, "n = %lld outside [1, 2^31-1]", (long long)n);
+    if (!x || (model == FM_ECM && !y)) return fail(FM_ERR_INVALID, "x (and, for the ECM, y) needed");
+    if (model == FM_UBCM && y) return fail(FM_ERR_INVALID, "UBCM takes no y");
+    if (!nodes) n_nodes = n;
+    if (n_nodes < 0) return fail(FM_ERR_INVALID, "n_nodes < 0");
+    if (n_nodes == 0) return FM_OK;
+    if (!k && !kvar && !s && !svar) return FM_OK;
+    for (const void *o : {(const void *)k, (const void *)kvar, (const void *)s, (const void *)svar})
+        if (o && !is_device_ptr(o)) return fail(FM_ERR_INVALID, "outputs must be DEVICE buffers");
+    if (model == FM_UBCM && (s || svar)) return fail(FM_ERR_INVALID, "UBCM has no strengths");
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    Allocs tmp(st);
+    auto dev_copy = [&](const auto *h, int64_t cnt, const auto **d) -> cudaError_t {
+        *d = h;
+        if (!h || is_device_ptr(h)) return cudaSuccess;
+        using T = std::remove_const_t<std::remove_pointer_t<decltype(h)>>;
+        T *t;
+        cudaError_t e = tmp.get(&t, cnt);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(t, h, sizeof(T) * cnt, cudaMemcpyHostToDevice, st);
+        *d = t;
+        return e;
+    };
+    const double *xd, *yd;
+    const int32_t *nd;
+    CK(dev_copy(x, n, &xd), "copy x");
+    CK(dev_copy(y, n, &yd), "copy y");
+    CK(dev_copy(nodes, n_nodes, &nd), "copy nodes");
+    CK(launch_expected((int)model, n, xd, yd, nd, n_nodes, k, kvar, s, svar, st), "expected");
+    CK(cudaStreamSynchronize(st), "sync (expected)");
     return FM_OK;
 }
 

@@ -12,6 +12,7 @@ constexpr int kG = 16;                         // work unit: one expected draw =
 constexpr int64_t kUnit = int64_t(1) << kG;
 constexpr uint32_t kPlanMagic = 0x4C504D46u;   // "FMPL"
 constexpr uint32_t kOwnerMagic = 0x57504D46u;  // "FMPW"
+constexpr int kMaxDevices = 64;
 
 // device-side error flags (atomicOr)
 enum : uint32_t {
@@ -70,6 +71,10 @@ struct Plan {
     int64_t cap_per_sample;  // scratch edges per sample (upper bound of chunk_cap[n_chunks])
     bool slots_aligned;      // every scratch slot starts at a multiple of 4 edges (32 bytes)
     unsigned int *dev_flags; // planner invariant flags (checked by fm_sample_*)
+    // capacity hint for the final edge list of a call (a performance hint, never a result):
+    // edges per sample <= out_ratio * (est_draws - n_seg) + margin; raised when a call overflows,
+    // lowered to the observed ratio (+1 %) otherwise.  Guarded by the library's object mutex.
+    double out_ratio;
 };
 
 struct Owner {
@@ -155,6 +160,10 @@ cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, voi
 // reverse inclusive max: out[t] = max(in[t], out[t+1]), out[n] = 0.0 (out has n+1 entries)
 cudaError_t suffix_max_f64(const double *in, double *out, int64_t n, void *tmp, size_t tmp_bytes,
                            cudaStream_t st);
+
+// closed-form expectations k, kvar (and ECM s, svar) of the listed nodes (fm_expect.cu, T1)
+cudaError_t launch_expected(int model, int64_t n, const double *x, const double *y, const int32_t *nodes,
+                            int64_t n_nodes, double *k, double *kvar, double *s, double *svar, cudaStream_t st);
 
 // radix sort (fm_sort.cu): sort (key, val) pairs ascending by key, stable.  Buffers are
 // ping-ponged; on return *key_out/*val_out point to the sorted arrays (one of the two buffers).

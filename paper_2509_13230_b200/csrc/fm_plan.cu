@@ -368,3 +368,15 @@ __global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap)
 }
 
 }  // namespace fm
+
+namespace fm {
+// test hook (FM_DEBUG_BAD_BOUND, fm_capi.cu): every segment record's initial bound numerator x0
+// scaled by f (q0 = x0 / d0 shrinks below p of the first candidates: a contract violation)
+__global__ void k_debug_scale_bound(unsigned char *rec, int64_t n_seg, int stride, double f)
+{
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_seg) return;
+    SegRec *r = reinterpret_cast<SegRec *>(rec + (size_t)g * stride);
+    r->x0 = __dmul_rn(r->x0, f);
+}
+}  // namespace fm

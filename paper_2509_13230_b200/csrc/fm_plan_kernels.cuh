@@ -53,6 +53,9 @@ __global__ void k_excl(int64_t n, const int32_t *perm, const int32_t *crank, int
 __global__ void k_chunks(int64_t n_seg, int64_t n_chunks, int64_t target, const int64_t *work_pre, int64_t *chunk_seg,
                          int64_t *chunk_cap);
 __global__ void k_fill_caps(int64_t *chunk_cap, int64_t n_chunks, int64_t cap);
+// test hook (FM_DEBUG_BAD_BOUND): scale every segment's initial bound numerator x0 by `f` so that
+// the first candidates violate p <= q -- exercises the FM_DEBUG_CHECKS path (FM_ERR_BOUND)
+__global__ void k_debug_scale_bound(unsigned char *rec, int64_t n_seg, int stride, double f);
 __global__ void k_pack_cand(int model, int64_t nc, const double *ckappa, const int32_t *cperm, const double *cy,
                             const double *cly, double2 *cand);
 
@@ -131,6 +134,7 @@ struct SampleArgs {
     int64_t *spill_off;            // [n_tasks] spill region of each task: -1 none, -2 failed
     unsigned long long *counters;  // draws, landed, accepted
     unsigned int *flags;
+    int check;                     // FM_DEBUG_CHECKS: test p <= q (1 + 2^-50) at every landed candidate
     // statistics mode (fm_sample_degrees, NEXT-3): when deg_row != NULL no edge list is written;
     // accepted edges add 1 (and w) to the row node's and the candidate's sums instead
     unsigned long long *deg_row, *deg_col, *str_row, *str_col;

@@ -101,13 +101,18 @@ __device__ __forceinline__ uint32_t load_logtab()
 // only: the scratch edge holds (row id, candidate RANK) and the compaction maps the rank to its id
 // (the id gather leaves the latency-bound chain for the bandwidth-bound copy).
 // kOrdered: bipartite / directed output (row id, candidate id) as is (R16).
-template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered>
+// kCheck (FM_DEBUG_CHECKS=1): every landed candidate checks the contract p <= q (1 + 2^-50)
+// (DESIGN R13) and flags kErrBound -- the call then fails with FM_ERR_BOUND.
+template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
     // rarely used per-chain task state lives in shared memory (registers are the occupancy limit)
     __shared__ int64_t s_task[kThreads * kC];   // current task id, -1 none
     __shared__ int64_t s_spill[kThreads * kC];  // its spill region: -1 none, -2 failed
+    // 64-bit per-thread draw / accepted counters: the 32-bit registers below are added here at
+    // every task end (a statistics call over many samples passes 2^32 per warp)
+    __shared__ unsigned long long s_ndraw[kThreads], s_nacc[kThreads];
     // UBCM: the last < 4 accepted edges of each lane's slot, so that the slot is written in whole
     // 32-byte sectors (structure of arrays: conflict-free)
     __shared__ int2 s_eb[kModel == FM_UBCM ? 4 : 1][kThreads];
@@ -157,7 +162,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // draws; landed = draws - segments and accepted = edges are derived by the host (every
     // segment ends with exactly one terminal draw); statistics mode counts accepted edges
     uint32_t n_draw = 0, n_acc = 0;
-    bool wsat = false;
+    s_ndraw[threadIdx.x] = 0;
+    s_nacc[threadIdx.x] = 0;
+    bool wsat = false, bad_bound = false;
 
     // segment g[c] of chain c's task becomes current (64/96-byte record; the record of the next
     // segment is prefetched into this chain's shared-memory slot with cp.async)
@@ -288,6 +295,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                         A.spill_off[tk] = s_spill[ci];
                     }
                     s_task[ci] = -1;
+                    s_ndraw[threadIdx.x] += n_draw;
+                    s_nacc[threadIdx.x] += n_acc;
+                    n_draw = n_acc = 0;
                 }
             }
             const uint32_t nc = __ballot_sync(0xffffffffu, needc && !warp_done);
@@ -440,6 +450,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     const double D = __dadd_rn(1.0, X);
                     const double hn = fm_log1p(X, T);
                     if (landed[c]) {  // accept iff u < (X/D) / (xq/dq), cross-multiplied (R10)
+                        if (kCheck && __dmul_rn(X, dq[c]) > __dmul_rn(__dmul_rn(xq[c], D), 1.0 + 0x1p-50))
+                            bad_bound = true;  // p > q (1 + 2^-50): the bound is violated
                         acc[c] = __dmul_rn(__dmul_rn(U01(w_land[c]), xq[c]), D) < __dmul_rn(X, dq[c]);
                         xq[c] = X;
                         dq[c] = D;
@@ -468,6 +480,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     }
                     const double hn = fm_log1p(__dmul_rn(z, iomb), T);
                     if (landed[c]) {
+                        if (kCheck && __dmul_rn(z, dq[c]) > __dmul_rn(__dmul_rn(xq[c], Dp), 1.0 + 0x1p-50))
+                            bad_bound = true;  // p > q_hat (1 + 2^-50)
                         acc[c] = __dmul_rn(__dmul_rn(U01(w_land[c]), xq[c]), Dp) < __dmul_rn(z, dq[c]);
                         xq[c] = z;
                         dq[c] = __dadd_rn(omb, z);
@@ -568,13 +582,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         }
     }
 #endif
+    if (kCheck && __any_sync(0xffffffffu, bad_bound) && lane == 0) atomicOr(A.flags, kErrBound);
     if (A.rerun_base) return;
-    const unsigned dr = __reduce_add_sync(0xffffffffu, n_draw);
-    const unsigned ac = __reduce_add_sync(0xffffffffu, n_acc);
+    unsigned long long dr = s_ndraw[threadIdx.x] + n_draw, ac = s_nacc[threadIdx.x] + n_acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dr += __shfl_xor_sync(0xffffffffu, dr, o);
+        ac += __shfl_xor_sync(0xffffffffu, ac, o);
+    }
     const bool anysat = __any_sync(0xffffffffu, wsat);
     if (lane == 0) {
-        atomicAdd(&A.counters[0], (unsigned long long)dr);
-        if (kStats) atomicAdd(&A.counters[2], (unsigned long long)ac);
+        atomicAdd(&A.counters[0], dr);
+        if (kStats) atomicAdd(&A.counters[2], ac);
         if (anysat) atomicOr(A.flags, kFlagWeightSat);
     }
 }
@@ -807,17 +826,23 @@ cudaError_t ensure_log_table(cudaStream_t st)
 
 // one instantiation per (model, statistics mode, ECM bound refresh, UBCM gather record, output
 // orientation); kMinB = 3 blocks per SM
-template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered>
+template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
-    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kGather, kOrdered>;
+    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kGather, kOrdered, kCheck>;
     int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err != cudaSuccess) return err;
     const size_t dyn = (size_t)kThreads * kC * (kModel == FM_ECM ? 96 : 64);
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    // function attributes are per device: set once per (instantiation, device), thread-safe
+    static std::mutex attr_mu;
+    static bool attr_set[kMaxDevices] = {};
+    std::lock_guard<std::mutex> attr_lk(attr_mu);
+    if (dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    if (!attr_set[dev]) {
+        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (err != cudaSuccess) return err;
         // shared-memory carveout (percent of the unified L1/shared capacity): the driver's default
         // picked 135 KB of shared memory for 3 x 27 KB of need; 40 % leaves more L1 for the kappa /
         // perm gathers (UBCM kernel -1 %; 0 % starves occupancy: +70 %).  FM_SAMPLE_CARVEOUT
@@ -831,10 +856,14 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
             const int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
             carve = std::max(carve, std::min(pct, 100));
         }
-        if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-        attr_set = true;
+        if (carve >= 0) {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            if (err != cudaSuccess) return err;
+        }
+        attr_set[dev] = true;
     }
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+    if (err != cudaSuccess) return err;
     int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
     const int64_t need = (a.n_tasks + kThreads * kC - 1) / (kThreads * kC);  // <= one task per chain at start
     if (need < blocks) blocks = need;
@@ -843,15 +872,23 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
     return cudaGetLastError();
 }
 
-template <int kModel, bool kStats, bool kRefresh, int kGather>
-static cudaError_t launch_sample_o(const SampleArgs &a, cudaStream_t st)
+template <int kModel, bool kStats, bool kRefresh, int kGather, bool kCheck>
+static cudaError_t launch_sample_c(const SampleArgs &a, cudaStream_t st)
 {
     constexpr int kMinB = kModel == FM_ECM ? FM_SAMPLE_MINB_ECM
                           : kGather == 2   ? FM_SAMPLE_MINB_RANKOUT : FM_SAMPLE_MINB_UBCM;
     // statistics mode writes no pairs: its orientation is irrelevant
     if constexpr (!kStats)
-        if (kGather != 2 && a.ordered) return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, true>(a, st);
-    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, false>(a, st);
+        if (kGather != 2 && a.ordered)
+            return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, true, kCheck>(a, st);
+    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, false, kCheck>(a, st);
+}
+
+template <int kModel, bool kStats, bool kRefresh, int kGather>
+static cudaError_t launch_sample_o(const SampleArgs &a, cudaStream_t st)
+{
+    return a.check ? launch_sample_c<kModel, kStats, kRefresh, kGather, true>(a, st)
+                   : launch_sample_c<kModel, kStats, kRefresh, kGather, false>(a, st);
 }
 
 cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)

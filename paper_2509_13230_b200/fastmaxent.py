@@ -30,7 +30,7 @@ STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ER
 FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
 _KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
 SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_sample_ecm_ex", "fm_edges_to_host", "fm_plan_get_info",
-           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval"]
+           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval", "fm_expected_degrees"]
 
 
 class FastMaxEntError(RuntimeError):
@@ -81,6 +81,8 @@ def _load():
     L.fm_sample_degrees.restype = C.c_int
     L.fm_sample_richclub.argtypes = [vp, u64, i64, i64, vp, vp, C.POINTER(_Counters)]
     L.fm_sample_richclub.restype = C.c_int
+    L.fm_expected_degrees.argtypes = [C.c_int, i64, vp, vp, vp, i64, vp, vp, vp, vp, vp]
+    L.fm_expected_degrees.restype = C.c_int
     L.fm_edges_to_host.argtypes = [C.POINTER(_Edges), vp, vp, vp]
     L.fm_edges_to_host.restype = C.c_int
     L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
@@ -357,6 +359,31 @@ def sample_richclub(plan: Plan, seed: int, n_samples: int = 1, first_sample: int
     _check(lib.fm_sample_richclub(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
                                   _stream(stream), C.c_void_p(e.data_ptr()), C.byref(c)))
     return e, {"draws": c.draws, "landed": c.landed, "accepted": c.accepted, "flags": c.flags}
+
+
+def expected_degrees(x, y=None, nodes=None, stream=None):
+    """fm_expected_degrees: exact per-node sum_j p_ij and sum_j p_ij (1 - p_ij) (and, for
+    the ECM, the expected strength and its variance) of the listed node ids (None: all nodes).
+    Returns (k, kvar, s, svar) as CUDA float64 tensors (s, svar None for the UBCM)."""
+    import torch
+    px, kx, n = _as_f64(x)
+    py, ky = (None, None) if y is None else _as_f64(y)[:2]
+    keep_nodes = None
+    m = n
+    pn = None
+    if nodes is not None:
+        if isinstance(nodes, torch.Tensor):
+            keep_nodes = nodes.to(torch.int32).contiguous()
+            pn = C.c_void_p(keep_nodes.data_ptr())
+        else:
+            keep_nodes = np.ascontiguousarray(nodes, dtype=np.int32)
+            pn = C.c_void_p(keep_nodes.ctypes.data)
+        m = int(keep_nodes.numel() if isinstance(keep_nodes, torch.Tensor) else keep_nodes.size)
+    out = [torch.empty(m, dtype=torch.float64, device="cuda") for _ in range(2 if y is None else 4)]
+    ptr = [C.c_void_p(t.data_ptr()) for t in out] + [None] * (4 - len(out))
+    _check(lib.fm_expected_degrees(FM_UBCM if y is None else FM_ECM, n, px, py, pn, m, *ptr, _stream(stream)))
+    del kx, ky, keep_nodes
+    return (out[0], out[1], None, None) if y is None else tuple(out)
 
 
 def abi_version() -> int:

@@ -76,3 +76,40 @@ def degree_sums(offsets, edges, n, weights=None):
             s = np.bincount(e[:, 0], weights=w, minlength=n) + np.bincount(e[:, 1], weights=w, minlength=n)
             s1 += s; s2 += s * s
     return k1, k2, s1, s2
+
+
+def node_gate(D, k, kv, R, alpha=1e-3, sigma=5.0):
+    """Per-node statistical gate on ensemble sums.
+
+    D: per-node sum over R samples of the degree (or strength); the exact law has mean R k and
+    variance R kv (independent pairs).  Nodes with R kv >= 25: z = (D - R k)/sqrt(R kv)
+    must satisfy |z| < zc with zc = sigma for m <= 1000 tested nodes (the north star's 5 sigma;
+    family-wise error ~6e-4) and the Bonferroni zc = Phi^-1(1 - alpha/(2m)) beyond (6.1 at m = 1e6).
+    Nodes with 0 < R kv < 25 (non-normal): two-sided tail of Poisson(R k) -- heavier-tailed than
+    the Poisson-binomial of the same mean -- must exceed alpha/(2m).  kv == 0: D == R k exactly.
+    Aggregate: sum of z^2 over the normal nodes within 6 sqrt(2 m') of its mean m'.
+    Returns a dict of diagnostics; raises AssertionError on failure."""
+    D = np.asarray(D, np.float64)
+    k = np.asarray(k, np.float64)
+    kv = np.asarray(kv, np.float64)
+    m = len(D)
+    zc = sigma if m <= 1000 else max(sigma, float(stats.norm.isf(alpha / (2 * m))))
+    big = R * kv >= 25
+    z = (D[big] - R * k[big]) / np.sqrt(R * kv[big])
+    zmax = float(np.max(np.abs(z))) if z.size else 0.0
+    assert zmax < zc, f"max |z| = {zmax:.2f} >= {zc:.2f} over {int(big.sum())} nodes"
+    small = (~big) & (kv > 0)
+    if small.any():
+        lam = R * k[small]
+        lo = stats.poisson.cdf(D[small], lam)
+        hi = stats.poisson.sf(D[small] - 1, lam)
+        pmin = float(np.min(np.minimum(lo, hi)))
+        assert pmin > alpha / (2 * m), f"low-variance node tail p = {pmin:.3g}"
+    zero = kv == 0
+    if zero.any():
+        assert np.allclose(D[zero], R * k[zero], rtol=0, atol=1e-6), "deterministic nodes"
+    mm = int(big.sum())
+    agg = float(np.sum(z * z))
+    if mm:
+        assert abs(agg - mm) < 6 * np.sqrt(2 * mm), f"sum z^2 = {agg:.1f} for {mm} nodes"
+    return {"nodes": m, "normal": mm, "zmax": zmax, "zc": zc, "sum_z2": agg}

@@ -38,6 +38,13 @@ def test_argument_validation_without_device():
     assert lib.fm_sort_plan(0, 4, C.cast(x, C.c_void_p), None, 5, None, C.byref(h)) == fm.FM_ERR_INVALID  # S < 8
     st = fm._Edges()
     assert lib.fm_sample_ubcm(None, 1, 0, 1, None, C.byref(st)) == fm.FM_ERR_STATE
+    # fm_expected_degrees: argument checks come before any device access
+    assert lib.fm_expected_degrees(0, 0, C.cast(x, C.c_void_p), None, None, 0, None, None, None, None,
+                                   None) == fm.FM_ERR_INVALID
+    assert lib.fm_expected_degrees(0, 1, C.cast(x, C.c_void_p), C.cast(x, C.c_void_p), None, 1, None, None,
+                                   None, None, None) == fm.FM_ERR_INVALID  # UBCM takes no y
+    assert lib.fm_expected_degrees(1, 1, C.cast(x, C.c_void_p), None, None, 1, None, None, None, None,
+                                   None) == fm.FM_ERR_INVALID  # ECM needs y
     lib.fm_free(None)  # no-op
 
 

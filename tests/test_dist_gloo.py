@@ -68,3 +68,22 @@ def test_gloo_world2_shards_equal_single_run(tmp_path, O):
             ra, rb = ref.offsets[3 * r + s], ref.offsets[3 * r + s + 1]
             assert np.array_equal(np.array(e[a:b]).reshape(-1, 2), ref.edges[ra:rb])
             assert np.array_equal(np.array(w[a:b]), ref.weights[ra:rb])
+
+
+def test_bench_self_launches_n_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (here with the gloo
+    self-test of its rank logic: shards, max over ranks, sums; no GPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest-dist"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 only
+    r = lines[0]
+    R = WL.workload(5).n_samples
+    assert r["n_gpus"] == 2 and r["samples_per_rank"] == R
+    assert r["first_samples"] == [0, R] and r["t_max"] == 11.0 and r["edges_all"] == 3000
