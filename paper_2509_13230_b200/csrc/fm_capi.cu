@@ -22,6 +22,9 @@ void dump_trace();  // fm_sample.cu (timeline instrumentation build)
 }
 #endif
 namespace fm {
+void fuse_stats_dump();  // fm_sample.cu (FM_FUSE_STATS instrumentation build; no-op otherwise)
+}
+namespace fm {
 std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches += n; }
 }  // namespace fm
@@ -632,8 +635,16 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         // segment records come from DRAM once per launch instead of once per sample (sampler
         // -2.2 % on config 4, -1.9 % on config 5; +1 % (UBCM) / +2.6 % (ECM) at N = 1e5, where
         // the records stay in L2 anyway: off there).  Results do not depend on it.
+        // v3 fused write (UBCM, opt-in FM_FUSE_WRITE=1): one block per SM whose warp 0
+        // copies the block's finished task batches into the final list (TMA bulk copies through shared
+        // memory, decoupled look-back offsets, L2 discard of the scratch) while 23 warps sample.  Measured
+        // at parity with the separate compaction, not faster (the copier warp is issue-starved next to
+        // 23 sampler warps; the sampler loses a warp), so the default stays the compaction pass.
+        const bool fuse = model == FM_UBCM && p->slots_aligned && env_i64("FM_FUSE_WRITE", 0) != 0 &&
+                          (!a.rank_out || env_i64("FM_FUSE_RANKOUT", 0) != 0);
         a.il_s[0] = a.il_s[1] = 0;
-        if (p->nc >= env_i64("FM_INTERLEAVE_MIN", int64_t(1) << 19)) {
+        // (the fused copy needs batches of consecutive canonical tasks: sample-major queue)
+        if (!fuse && p->nc >= env_i64("FM_INTERLEAVE_MIN", int64_t(1) << 19)) {
             a.il_s[0] = tm.s_split;
             a.il_s[1] = n_samples - tm.s_split;
             if (a.il_s[0] == 0) a.il_s[0] = 1;  // range 0 empty: never indexed
@@ -656,22 +667,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         a.counters = hd->counters;
         a.flags = &hd->flags;
         a.check = env_i64("FM_DEBUG_CHECKS", 0) != 0;
-        PhaseTimer ts, tw;
-        ts.begin(kPhaseSample, st);
-        CK(launch_sample(model, a, st), "sampler launch");
-        ts.end(st);
-        tw.begin(kPhaseWrite, st);
-        if (g_timing.load()) {
-            std::lock_guard<std::mutex> lk(g_tmu);
-            g_sample_launches++;
-        }
-        CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
-        CK(launch_offsets(n_samples, tm, dest, offs_d, st), "offsets");
-        CK(launch_overflow(n_tasks, tm, counts, spill_off, &hd->n_overflow, ovl, st), "overflow check");
-        // The final list is allocated up front (so compaction and the re-run of overflowed tasks are
-        // queued without a host round trip; one synchronisation at the end) with the plan's capacity
-        // hint: out_ratio x (estimated draws - segments) per sample + 8 sigma-like margin, at most the
-        // scratch's capacity.  A call whose edges exceed it redoes the write into an exact-size list.
+        // capacity of the final list: the plan's hint (see the end of this block), at most the scratch's
         int64_t out_cap = slots + spill_cap;
         {
             double ratio;
@@ -689,6 +685,23 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                 e = cudaMallocAsync(&own->weights, sizeof(int32_t) * std::max<int64_t>(cap, 1), st);
             return e;
         };
+        auto free_out = [&]() {
+            if (own->edges) cudaFreeAsync(own->edges, st);
+            if (own->weights) cudaFreeAsync(own->weights, st);
+            own->edges = own->weights = nullptr;
+        };
+        // fused-write bookkeeping: one look-back status word per queue batch of kQueueBatch tasks
+        const int64_t n_groups = (n_tasks + kQueueBatch - 1) / kQueueBatch;
+        unsigned long long *grp_state = nullptr;
+        if (fuse) {
+            CK(tmp.get(&grp_state, n_groups), "alloc batch states");
+            a.fuse = 1;
+            a.n_groups = n_groups;
+            a.grp_state = grp_state;
+            a.dest = dest;
+            a.discard = env_i64("FM_DISCARD", 1) != 0;
+            a.rank_map = a.rank_out ? p->cperm : nullptr;
+        }
         auto write_out = [&](int64_t cap, bool compact, bool rerun) -> cudaError_t {
             cudaError_t e = compact ? launch_compact(cap, n_tasks, tm, counts, dest, spill_off, se, sw, a.spill_e,
                                                      a.spill_w, (int2 *)own->edges, (int32_t *)own->weights,
@@ -696,6 +709,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                                     : cudaSuccess;
             if (e != cudaSuccess || !rerun) return e;
             SampleArgs r = a;  // deterministic re-run of overflowed tasks straight into the final list
+            r.fuse = 0;
             r.n_tasks = n_tasks;
             r.n_tasks_dev = &hd->n_overflow;
             r.task_list = ovl;
@@ -705,20 +719,50 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             r.weights = (int32_t *)own->weights;
             return launch_sample(model, r, st);
         };
-        // the re-run of overflowed tasks (rare) is launched only after the synchronisation shows one
-        CK(alloc_out(out_cap), "alloc edges");
-        CK(write_out(out_cap, true, false), "compact");
-        CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
-           "read offsets");
-        CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+        // one pass of the call: sampler (+ copiers), offsets, overflow list; the host learns the total
+        // at the one synchronisation
+        auto run_pass = [&](int64_t cap) -> fm_status {
+            CK(alloc_out(cap), "alloc edges");
+            PhaseTimer ts, tw;
+            if (fuse) {
+                CK(cudaMemsetAsync(grp_state, 0, sizeof(unsigned long long) * n_groups, st), "memset batch states");
+                CK(cudaMemsetAsync(hd, 0, sizeof(Hdr), st), "memset hdr");
+                a.out_e = (int2 *)own->edges;
+                a.out_w = (int32_t *)own->weights;
+                a.out_cap = cap;
+            }
+            ts.begin(kPhaseSample, st);
+            CK(launch_sample(model, a, st), "sampler launch");
+            ts.end(st);
+            tw.begin(kPhaseWrite, st);
+            if (g_timing.load()) {
+                std::lock_guard<std::mutex> lk(g_tmu);
+                g_sample_launches++;
+            }
+            if (!fuse) CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
+            CK(launch_offsets(n_samples, tm, dest, offs_d, st), "offsets");
+            CK(launch_overflow(n_tasks, tm, counts, spill_off, &hd->n_overflow, ovl, st), "overflow check");
+            // the final list was allocated up front (compaction and the re-run of overflowed tasks are
+            // queued without a host round trip; one synchronisation at the end)
+            if (!fuse) CK(write_out(cap, true, false), "compact");
+            CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
+               "read offsets");
+            CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+            tw.end(st);
+            CK(cudaStreamSynchronize(st), "sync (sample)");
+            return FM_OK;
+        };
         unsigned int plan_flags = 0;
         CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
            "read plan flags");
-        tw.end(st);
-        CK(cudaStreamSynchronize(st), "sync (sample)");
+        {
+            fm_status r = run_pass(out_cap);
+            if (r != FM_OK) return r;
+        }
 #ifdef FM_TRACE
         fm::dump_trace();
 #endif
+        fm::fuse_stats_dump();
         if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
         // FM_DEBUG_CHECKS: a p > q contract violation fails the call; nothing stays allocated
         if (h.flags & kErrBound) return fail(FM_ERR_BOUND, "p > q (1 + 2^-50) detected at a landed candidate (S:L289)");
@@ -731,14 +775,22 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             if (total > out_cap) pm->out_ratio = std::max(pm->out_ratio, seen * 1.02);
             else if (n_samples >= 8) pm->out_ratio = std::max(seen * 1.01, 0.05);
         }
-        if (total > out_cap) {  // (pathological overflow) redo the write into an exact-size list
-            cudaFreeAsync(own->edges, st);
-            if (own->weights) cudaFreeAsync(own->weights, st);
-            own->edges = own->weights = nullptr;
+        if (total > out_cap) {  // the list was too small: redo the write into an exact-size list
+            free_out();
             out_cap = total;
-            CK(alloc_out(out_cap), "alloc edges");
-            CK(write_out(out_cap, true, h.n_overflow > 0), "compact / rerun");
-            CK(cudaStreamSynchronize(st), "sync (sample, exact)");
+            if (fuse) {  // the copiers consumed (discarded) the scratch: run the whole call again
+                fm_status r = run_pass(out_cap);
+                if (r != FM_OK) return r;
+                if (offsets_h[n_samples] != total) return fail(FM_ERR_STATE, "re-run total differs");
+                if (h.n_overflow > 0) {
+                    CK(write_out(out_cap, false, true), "rerun");
+                    CK(cudaStreamSynchronize(st), "sync (sample, rerun)");
+                }
+            } else {
+                CK(alloc_out(out_cap), "alloc edges");
+                CK(write_out(out_cap, true, h.n_overflow > 0), "compact / rerun");
+                CK(cudaStreamSynchronize(st), "sync (sample, exact)");
+            }
         } else if (h.n_overflow > 0) {
             CK(write_out(out_cap, false, true), "rerun");
             CK(cudaStreamSynchronize(st), "sync (sample, rerun)");

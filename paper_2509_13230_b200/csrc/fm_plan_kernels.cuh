@@ -102,6 +102,9 @@ __device__ __forceinline__ void task_decode(const TaskMap &M, int64_t t, int64_t
     }
 }
 
+// tasks per claim of the sampler's global queue (a warp batch; the fused write's unit)
+constexpr int kQueueBatch = 64;
+
 struct SampleArgs {
     const unsigned char *rec;      // segment records, stride kRecStride(model)
     const double *kappa_s, *y_s, *ly_s;  // CANDIDATE arrays (the - set; the rows themselves if undirected)
@@ -135,6 +138,16 @@ struct SampleArgs {
     unsigned long long *counters;  // draws, landed, accepted
     unsigned int *flags;
     int check;                     // FM_DEBUG_CHECKS: test p <= q (1 + 2^-50) at every landed candidate
+    // v3 fused write (fm_sample.cu: copier_loop): a copier warp per block copies the finished queue
+    // batches (kQueueBatch canonical tasks) from the scratch slots into the final list
+    int fuse;
+    int discard;                   // discard.global.L2 of a batch's scratch lines after its copy
+    int64_t n_groups;              // queue batches
+    unsigned long long *grp_state; // [n_groups] look-back status (flag bits | edge count / prefix)
+    int64_t *dest;                 // [n_tasks + 1] final offset of each task (dest[n_tasks] = total)
+    int2 *out_e;                   // final list (capacity out_cap)
+    int32_t *out_w;
+    const int32_t *rank_map;       // UBCM rank-out: candidate rank -> id
     // statistics mode (fm_sample_degrees, NEXT-3): when deg_row != NULL no edge list is written;
     // accepted edges add 1 (and w) to the row node's and the candidate's sums instead
     unsigned long long *deg_row, *deg_col, *str_row, *str_col;

@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "fm_internal.cuh"
 #include "fm_math.cuh"
@@ -64,7 +65,7 @@ namespace {
 #define FM_SAMPLE_MINB_RANKOUT 4
 #endif
 constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
-constexpr int kBatch = 64;  // tasks per warp batch
+constexpr int kBatch = kQueueBatch;  // tasks per warp batch
 
 // per-block copy of the log table: (invc, logc) pairs, one 16-byte lookup (8 conflict-free
 // copies, one per bank group, measured no faster: the lookups are not the bottleneck)
@@ -93,6 +94,712 @@ __device__ __forceinline__ uint32_t load_logtab()
     return base;
 }
 
+// ------------------------------------------------------------------------------------------
+// v3 fused write (a6 without the compaction pass), warp-specialised.  In a fused launch every
+// block has kThreads/32 - 1 SAMPLER warps and one COPIER warp.  Sampler warps claim the task
+// queue in batches of kBatch consecutive canonical tasks (every task of a batch runs on a lane of
+// the claiming warp) and register each batch in their block's ring (shared memory).  A lane that
+// finishes a task adds (1 task, its edge count) to its batch's packed counter; the lane that
+// finishes a batch's last task publishes the batch's edge count in the batch's global status word
+// (decoupled look-back: 2 flag bits + 62-bit value; batch 0 publishes its inclusive prefix).  The
+// copier warp takes the finished batches of its block, forms each one's output offset by
+// look-back over the preceding batches (resumable: an unfinished predecessor is revisited
+// later), publishes the inclusive prefix, copies the batch's edges from the scratch slots --
+// written by its own block moments earlier, in the L2 -- into the final list with streaming
+// stores, discards the batch's scratch lines from the L2 (discard.global.L2: no write-back), and
+// frees the ring entry.  A sampler warp with no free ring entry leaves its idle lanes idle.
+// Deadlock-free: finished-batch counts are published by sampler lanes, so a look-back waits only
+// on unfinished batches, and those run on sampler warps that never wait.
+constexpr uint64_t kGrpAgg = 1ull << 62, kGrpInc = 2ull << 62, kGrpVal = (1ull << 62) - 1;
+constexpr int kBRing = 128;             // ring entries per block (one bit each in 64-bit masks)
+constexpr int kFuseThreads = 768;       // fused launch: one block per SM, 23 sampler warps + 1 copier (24 warps at 80 registers fill the register file: 6 per SMSP)
+constexpr int kPackShift = 40;          // packed batch counter: finished tasks << 40 | edges
+#ifndef FM_COPY_JOBS
+#define FM_COPY_JOBS 8
+#endif
+#ifndef FM_COPY_JOBS_RANKOUT
+#define FM_COPY_JOBS_RANKOUT 4
+#endif
+
+// The status words carry only their own value (no data is published through them: a copier
+// copies its own block's batches, ordered by CTA-scope fences), so relaxed gpu-scope accesses
+// suffice -- an acquire load would invalidate the SM's whole L1 (CCTL.IVALL) at every poll.
+__device__ __forceinline__ uint64_t ld_status(const unsigned long long *p)
+{
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long *p, uint64_t v)
+{
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void discard_l2_line(const void *p)
+{
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// fused-write instrumentation (FM_FUSE_STATS builds): copies, copy cycles, polls without progress,
+// entries finished but blocked per poll, ring-full claim failures, sampler idle iterations
+#ifdef FM_FUSE_STATS
+__device__ unsigned long long g_fstats[8];
+#define FSTAT(i, v) atomicAdd(&g_fstats[i], (unsigned long long)(v))
+#else
+#define FSTAT(i, v) ((void)0)
+#endif
+
+// a task of the sub-batch being copied (per-copier table in shared memory)
+struct __align__(16) CopyDesc {
+    long long src, dst;  // slot start (scratch element index), final position
+    long long sp;        // spill region (-1 none)
+    int cnt, cap, jexcl, pad;
+};
+
+// the block's ring of claimed batches and the copier's staging buffer (shared memory); the
+// non-fused kernels get a minimal instance (no static shared memory for a copier they do not have)
+template <int NR, int NS>
+struct RingT {
+    unsigned long long packed[NR];  // finished tasks << kPackShift | their edges
+    long long b[NR];                // batch id, -1 free
+    long long lb_j[NR];             // resumable look-back: next predecessor to read (-2: none yet)
+    unsigned long long lb_pre[NR];  //   and the sum collected so far
+    unsigned long long free_mask[NR > 64 ? NR / 64 : 1];  // free entries
+    unsigned exited;                // sampler warps that have left the loop
+    unsigned long long mbar[2];     // the copier's bulk-load barriers (one per staging buffer)
+    CopyDesc desc[NR < 32 ? 1 : 32];  // the copier's sub-batch table (register-copy path)
+};
+using BlockRing = RingT<kBRing, 0>;
+
+// Copy the finished batch b (tasks [b kb, ...)) to the final list at `prefix`; write each task's
+// final offset.  Warp-synchronous.
+template <int kGather>
+__device__ __forceinline__ void batch_copy(const SampleArgs &A, int64_t b, int64_t prefix, int64_t agg, int kb,
+                                           CopyDesc *desc)
+{
+    const int lane = threadIdx.x & 31;
+    constexpr int kCopyJobs = kGather == 2 ? FM_COPY_JOBS_RANKOUT : FM_COPY_JOBS;
+    const int64_t T = A.n_tasks;
+    const int64_t t0 = b * kb, t1 = min(T, t0 + kb);
+    if (t1 == T && lane == 0) A.dest[T] = prefix + agg;
+    int64_t run = prefix;
+#ifdef FM_FUSE_STATS
+    long long ph0 = clock64(), ph_desc = 0, ph_jobs = 0;
+#endif
+    for (int64_t tb = t0; tb < t1; tb += 32) {
+        const int64_t t = tb + lane;
+        int64_t cnt = 0, src = 0, sp = -1, cap = 0;
+        if (t < t1) {
+            int64_t s_, c_;
+            int k_;
+            task_decode(A.tm, t, s_, c_, k_);
+            cap = A.tm.cap[k_][c_ + 1] - A.tm.cap[k_][c_];
+            src = s_ * A.tm.cap_per_sample + A.tm.cap[k_][c_];
+            cnt = A.counts[t];
+            sp = A.spill_off[t];
+        }
+        int64_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int64_t dst = run + incl - cnt;
+        if (t < t1) A.dest[t] = dst;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        // not copied: tasks whose data is incomplete (slot and spill overflowed: re-run after the
+        // kernel) and tasks beyond the list's capacity (the host then redoes the call)
+        const bool skip = (cnt > cap && (cnt > 2 * cap || sp < 0)) || dst + cnt > A.out_cap;
+        const int64_t ncp = skip ? 0 : cnt;
+        // jobs: 64 consecutive elements of one task, two per lane (16-byte loads: slots and spill
+        // regions start at multiples of 4 elements)
+        const int32_t nj = (int32_t)((ncp + 63) >> 6);
+        int32_t jincl = nj;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xffffffffu, jincl, o);
+            if (lane >= o) jincl += v;
+        }
+        const int32_t jexcl = jincl - nj;
+        const int32_t njobs = __shfl_sync(0xffffffffu, jincl, 31);
+        __syncwarp();
+        desc[lane].src = src;
+        desc[lane].dst = dst;
+        desc[lane].sp = sp;
+        desc[lane].cnt = (int32_t)ncp;
+        desc[lane].cap = (int32_t)cap;
+        desc[lane].jexcl = jexcl;
+        __syncwarp();
+#ifdef FM_FUSE_STATS
+        const long long ph1 = clock64();
+        ph_desc += ph1 - ph0;
+#endif
+        for (int32_t j0 = 0; j0 < njobs; j0 += kCopyJobs) {
+#ifdef FM_FUSE_STATS
+            if (lane == 0) FSTAT(5, 1);
+#endif
+            int4 v[kCopyJobs];
+            int64_t od[kCopyJobs];
+            int nv[kCopyJobs];
+#pragma unroll
+            for (int q = 0; q < kCopyJobs; q++) {
+                nv[q] = 0;
+                od[q] = 0;
+                const int32_t j = j0 + q;
+                if (j >= njobs) continue;  // warp-uniform
+                // the task holding job j: job prefixes increase strictly over the tasks with jobs,
+                // so it is the last such lane whose first job is <= j; its descriptor from the table
+                const int kk = 31 - __clz(__ballot_sync(0xffffffffu, jexcl <= j && nj > 0));
+                const CopyDesc &D = desc[kk];
+                const int64_t e = (int64_t)(j - D.jexcl) * 64 + 2 * lane;
+                const int64_t c_k = D.cnt, cap_k = D.cap, src_k = D.src, sp_k = D.sp, dst_k = D.dst;
+                if (e < c_k) {
+                    const int2 *q2 = e < cap_k ? A.edges + src_k + e : A.spill_e + sp_k + (e - cap_k);
+                    v[q] = *reinterpret_cast<const int4 *>(q2);
+                    nv[q] = e + 1 < c_k ? 2 : 1;
+                    od[q] = dst_k + e;
+                }
+            }
+            // every load of the round is issued before the first store (a compiler barrier: the
+            // loads would otherwise be sunk next to their stores, one latency each)
+            asm volatile("" ::: "memory");
+#ifdef FM_FUSE_STATS
+            const long long pl = clock64();
+#endif
+#pragma unroll
+            for (int q = 0; q < kCopyJobs; q++) {
+                if (nv[q] == 0) continue;
+                int2 e0 = make_int2(v[q].x, v[q].y), e1 = make_int2(v[q].z, v[q].w);
+                if (kGather == 2) {  // UBCM large N: (row id, candidate rank) -> (min id, max id)
+                    const int32_t i0 = __ldg(A.rank_map + e0.y);
+                    e0 = make_int2(min(e0.x, i0), max(e0.x, i0));
+                    if (nv[q] == 2) {
+                        const int32_t i1 = __ldg(A.rank_map + e1.y);
+                        e1 = make_int2(min(e1.x, i1), max(e1.x, i1));
+                    }
+                }
+                if (nv[q] == 2 && (od[q] & 1) == 0) {
+                    __stcs(reinterpret_cast<int4 *>(A.out_e + od[q]), make_int4(e0.x, e0.y, e1.x, e1.y));
+                } else {
+                    __stcs(A.out_e + od[q], e0);
+                    if (nv[q] == 2) __stcs(A.out_e + od[q] + 1, e1);
+                }
+            }
+#ifdef FM_FUSE_STATS
+            if (lane == 0) FSTAT(4, clock64() - pl);
+#endif
+        }
+#ifdef FM_FUSE_STATS
+        {
+            const long long ph2 = clock64();
+            ph_jobs += ph2 - ph1;
+            ph0 = ph2;
+        }
+#endif
+    }
+#ifdef FM_FUSE_STATS
+    if (lane == 0) {
+        FSTAT(6, ph_desc);
+        FSTAT(7, ph_jobs);
+    }
+#endif
+    // hand the batch's scratch lines back without a write-back: only whole 128-byte lines inside
+    // its slots (which no other task shares), after every lane's loads of them have completed
+    // (their values were stored above)
+    __syncwarp();
+    if (A.discard) {
+        const char *base = reinterpret_cast<const char *>(A.edges);
+        int64_t s_first, c_first, s_last, c_last;
+        int k_first, k_last;
+        task_decode(A.tm, t0, s_first, c_first, k_first);
+        task_decode(A.tm, t1 - 1, s_last, c_last, k_last);
+        for (int64_t s_ = s_first; s_ <= s_last; s_++) {
+            // the batch's tasks of sample s_ are consecutive chunks of one chunking: their slots
+            // form one contiguous range
+            const int kc = s_ == s_first ? k_first : s_ == s_last ? k_last : (s_ < A.tm.s_split ? 0 : 1);
+            const int64_t lo_c = s_ == s_first ? c_first : 0;
+            const int64_t hi_c = s_ == s_last ? c_last + 1 : A.tm.n_chunks[kc];
+            const size_t a = (size_t)(s_ * A.tm.cap_per_sample + A.tm.cap[kc][lo_c]) * sizeof(int2);
+            const size_t z = (size_t)(s_ * A.tm.cap_per_sample + A.tm.cap[kc][hi_c]) * sizeof(int2);
+            const size_t la = (a + 127) & ~(size_t)127, lz = z & ~(size_t)127;
+            for (size_t l = la + (size_t)lane * 128; l < lz; l += 32 * 128) discard_l2_line(base + l);
+        }
+    }
+}
+
+// ---- bulk asynchronous copies (TMA engine) for the copier: the data never passes through
+// registers, so the copier issues ~1 instruction per task instead of ~1 per 16 bytes (measured:
+// a register-copying warp next to 21 issue-bound sampler warps moved ~1 GB/s) ----
+__device__ __forceinline__ void mbar_init(uint32_t mbar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint32_t mbar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(mbar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void *src, unsigned bytes, uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src_smem, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+constexpr int kStageBytes = 16384;  // the copier's staging buffer (shared memory, BlockRing::stage)
+
+// Copy the finished batch b to the final list at `prefix` through the staging buffer with bulk
+// copies: per round, the lanes of the tasks that fit load their slot (+ spill) into the stage at
+// 16-byte-aligned offsets (one cp.async.bulk each, completing on the mbarrier); then tasks whose
+// final position is 16-byte aligned are stored by one bulk store each, the others by the warp
+// (pairs re-aligned through shared memory).  Writes each task's final offset.  Warp-synchronous.
+__device__ __forceinline__ void batch_copy_tma(const SampleArgs &A, int64_t b, int64_t prefix, int64_t agg, int kb,
+                                               uint32_t stage, uint32_t mbar, unsigned &phase)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t T = A.n_tasks;
+    const int64_t t0 = b * kb, t1 = min(T, t0 + kb);
+    if (t1 == T && lane == 0) A.dest[T] = prefix + agg;
+    const char *base = reinterpret_cast<const char *>(A.edges);
+    int64_t run = prefix;
+    for (int64_t tb = t0; tb < t1; tb += 32) {
+        const int64_t t = tb + lane;
+        int64_t cnt = 0, src = 0, sp = -1, cap = 0;
+        if (t < t1) {
+            int64_t s_, c_;
+            int k_;
+            task_decode(A.tm, t, s_, c_, k_);
+            cap = A.tm.cap[k_][c_ + 1] - A.tm.cap[k_][c_];
+            src = s_ * A.tm.cap_per_sample + A.tm.cap[k_][c_];
+            cnt = A.counts[t];
+            sp = A.spill_off[t];
+        }
+        int64_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int64_t dst = run + incl - cnt;
+        if (t < t1) A.dest[t] = dst;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+        const bool skip = (cnt > cap && (cnt > 2 * cap || sp < 0)) || dst + cnt > A.out_cap;
+        const int64_t ncp = skip ? 0 : cnt;
+        const int64_t n_slot = min(ncp, cap), n_sp = ncp - n_slot;
+        // staged bytes: the slot part (cap is a multiple of 4: a spilled slot part is whole 32-byte
+        // units) then the spill part, each rounded up to 16 bytes
+        const unsigned b_slot = (unsigned)(((n_slot + 1) & ~int64_t(1)) * 8);
+        const unsigned b_sp = (unsigned)(((n_sp + 1) & ~int64_t(1)) * 8);
+        const unsigned need = b_slot + b_sp;
+        // (a task larger than the stage -- only with very large seg_target -- is copied by the warp)
+        unsigned big = __ballot_sync(0xffffffffu, ncp > 0 && need > (unsigned)kStageBytes);
+        while (big) {
+            const int k = __ffs(big) - 1;
+            big &= big - 1;
+            const int64_t d_k = __shfl_sync(0xffffffffu, dst, k), c_k = __shfl_sync(0xffffffffu, ncp, k);
+            const int64_t s_k = __shfl_sync(0xffffffffu, src, k), p_k = __shfl_sync(0xffffffffu, sp, k);
+            const int64_t n_k = __shfl_sync(0xffffffffu, n_slot, k);
+            for (int64_t e = lane; e < c_k; e += 32)
+                __stcs(A.out_e + d_k + e, e < n_k ? A.edges[s_k + e] : A.spill_e[p_k + e - n_k]);
+        }
+        bool pending = ncp > 0 && need <= (unsigned)kStageBytes;
+        while (__any_sync(0xffffffffu, pending)) {
+            // this round: the pending tasks (in lane order) whose staging ranges fit
+            unsigned sz = pending ? need : 0u, inc = sz;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            const unsigned off = inc - sz;
+            // the first pending task always fits (a task's slot + spill is < kStageBytes)
+            const bool mine = pending && inc <= (unsigned)kStageBytes;
+            const unsigned total = __reduce_add_sync(0xffffffffu, mine ? sz : 0u);
+            // (the stage's previous contents have been read: order the async-proxy writes after)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lane == 0) mbar_arrive_expect(mbar, total);
+            __syncwarp();
+            if (mine) {
+                if (b_slot) bulk_g2s(stage + off, base + (size_t)src * 8, b_slot, mbar);
+                if (b_sp) bulk_g2s(stage + off + b_slot, A.spill_e + sp, b_sp, mbar);
+            }
+            mbar_wait(mbar, phase & 1);
+            phase++;
+            // the slot data is in shared memory: the scratch lines can be discarded (whole lines
+            // inside the slot only)
+            if (mine && A.discard && n_slot > 0) {
+                const size_t a = (size_t)src * 8, z = a + (size_t)cap * 8;
+                for (size_t l = (a + 127) & ~(size_t)127; l + 128 <= z; l += 128) discard_l2_line(base + l);
+            }
+            // aligned final position: one bulk store (the odd last element by the lane itself)
+            const bool even = (dst & 1) == 0;
+            if (mine && even) {
+                const unsigned nb = (unsigned)(ncp & ~int64_t(1)) * 8;
+                if (nb) bulk_s2g(A.out_e + dst, stage + off, nb);
+                if (ncp & 1) {
+                    // the element after the slot part's padding when spilled: staged contiguously
+                    // only if n_slot is even (spilled slot parts are multiples of 4), so index
+                    // ncp - 1 is at off + (ncp - 1) * 8 whenever n_sp == 0 or n_slot is even
+                    int2 e;
+                    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(stage + off + (unsigned)(ncp - 1) * 8));
+                    __stcs(A.out_e + dst + ncp - 1, e);
+                }
+            }
+            bulk_commit();
+            // odd final positions: the warp copies each such task, element 0 alone, then pairs
+            unsigned odd = __ballot_sync(0xffffffffu, mine && !even);
+            while (odd) {
+                const int k = __ffs(odd) - 1;
+                odd &= odd - 1;
+                const int64_t d_k = __shfl_sync(0xffffffffu, dst, k);
+                const int64_t c_k = __shfl_sync(0xffffffffu, ncp, k);
+                const unsigned o_k = __shfl_sync(0xffffffffu, off, k);
+                for (int64_t e0 = 2 * lane; e0 < c_k + 1; e0 += 64) {
+                    // output pair (d_k + e0 - 1, d_k + e0) for e0 >= 2 is 16-byte aligned; e0 = 0: element 0
+                    if (e0 == 0) {
+                        int2 e;
+                        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(stage + o_k));
+                        __stcs(A.out_e + d_k, e);
+                        continue;
+                    }
+                    int2 x0, x1 = make_int2(0, 0);
+                    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(x0.x), "=r"(x0.y) : "r"(stage + o_k + (unsigned)(e0 - 1) * 8));
+                    if (e0 < c_k) {
+                        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(x1.x), "=r"(x1.y) : "r"(stage + o_k + (unsigned)e0 * 8));
+                        __stcs(reinterpret_cast<int4 *>(A.out_e + d_k + e0 - 1), make_int4(x0.x, x0.y, x1.x, x1.y));
+                    } else {
+                        __stcs(A.out_e + d_k + e0 - 1, x0);
+                    }
+                }
+            }
+            // the stage is re-filled next round: the bulk stores must have read it
+            bulk_wait_read();
+            __syncwarp();
+            pending = pending && !mine;
+        }
+    }
+}
+
+// ---- the pipelined copy: sub-batches of 32 tasks (one per lane) alternate between two staging
+// buffers, so the bulk loads of one sub-batch overlap the stores of the previous one ----
+constexpr int kStageBuf = 40960;  // bytes per staging buffer (two buffers)
+struct SubDesc {
+    long long dst, src;  // final position, slot start (elements)
+    long long sp;        // spill region of a spilled task (copied by the warp), else -1
+    int ncp, cap;        // elements to copy, slot capacity
+    unsigned off;        // staging offset (bytes, 16-byte aligned)
+};
+
+// Descriptors of the sub-batch [tb, min(tb + 32, t1)) whose output starts at `run` (advanced past
+// it); writes the tasks' final offsets.  Returns the sub-batch's staged bytes (> kStageBuf: it
+// does not fit one buffer).
+__device__ __forceinline__ unsigned sub_prep(const SampleArgs &A, int64_t tb, int64_t t1, int64_t &run, SubDesc &d)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t t = tb + lane;
+    int64_t cnt = 0, src = 0, sp = -1, cap = 0;
+    if (t < t1) {
+        int64_t s_, c_;
+        int k_;
+        task_decode(A.tm, t, s_, c_, k_);
+        cap = A.tm.cap[k_][c_ + 1] - A.tm.cap[k_][c_];
+        src = s_ * A.tm.cap_per_sample + A.tm.cap[k_][c_];
+        cnt = A.counts[t];
+        sp = A.spill_off[t];
+    }
+    int64_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int64_t dst = run + incl - cnt;
+    if (t < t1) A.dest[t] = dst;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+    // not copied: incomplete tasks (slot and spill overflowed: re-run after the kernel) and tasks
+    // beyond the list's capacity (the host then redoes the call); spilled tasks (rare) are copied
+    // by the warp itself (sub_finish)
+    const bool skip = (cnt > cap && (cnt > 2 * cap || sp < 0)) || dst + cnt > A.out_cap;
+    const int64_t ncp = skip ? 0 : cnt;
+    const unsigned need = ncp > cap ? 0u : (unsigned)(((ncp + 1) & ~int64_t(1)) * 8);
+    unsigned inc = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    d.dst = dst;
+    d.src = src;
+    d.sp = ncp > cap ? sp : -1;
+    d.ncp = (int)ncp;
+    d.cap = (int)cap;
+    d.off = inc - need;
+    return __shfl_sync(0xffffffffu, inc, 31);
+}
+
+// spilled tasks of a sub-batch (slot + spill region, rare): plain warp copy
+__device__ __forceinline__ void sub_copy_spilled(const SampleArgs &A, const SubDesc &d, bool all)
+{
+    const int lane = threadIdx.x & 31;
+    unsigned spl = __ballot_sync(0xffffffffu, d.ncp > 0 && (all || d.sp >= 0));
+    while (spl) {
+        const int k = __ffs(spl) - 1;
+        spl &= spl - 1;
+        const long long d_k = __shfl_sync(0xffffffffu, d.dst, k);
+        const int c_k = __shfl_sync(0xffffffffu, d.ncp, k), cap_k = __shfl_sync(0xffffffffu, d.cap, k);
+        const long long sp_k = __shfl_sync(0xffffffffu, d.sp, k), src_k = __shfl_sync(0xffffffffu, d.src, k);
+        for (int e = lane; e < c_k; e += 32)
+            __stcs(A.out_e + d_k + e, e < cap_k ? A.edges[src_k + e] : A.spill_e[sp_k + e - cap_k]);
+    }
+}
+__device__ __forceinline__ void sub_finish_nowait(const SampleArgs &A, const SubDesc &d) { sub_copy_spilled(A, d, false); }
+__device__ __forceinline__ void sub_copy_plain(const SampleArgs &A, const SubDesc &d) { sub_copy_spilled(A, d, true); }
+
+// Bulk-load the sub-batch's slots into the staging buffer (one instruction per task).
+__device__ __forceinline__ void sub_issue(const SampleArgs &A, const SubDesc &d, uint32_t buf, uint32_t mbar,
+                                          unsigned total)
+{
+    const int lane = threadIdx.x & 31;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (lane == 0) mbar_arrive_expect(mbar, total);
+    __syncwarp();
+    if (d.ncp > 0 && d.sp < 0)
+        bulk_g2s(buf + d.off, reinterpret_cast<const char *>(A.edges) + (size_t)d.src * 8,
+                 (unsigned)((d.ncp + 1) & ~1) * 8, mbar);
+}
+
+// Wait for the sub-batch's loads, discard its scratch lines, store it: aligned final positions by
+// one bulk store per task, odd ones by the warp (pairs re-aligned through shared memory).
+__device__ __forceinline__ void sub_finish(const SampleArgs &A, const SubDesc &d, uint32_t buf, uint32_t mbar,
+                                           unsigned &phase)
+{
+    const int lane = threadIdx.x & 31;
+    mbar_wait(mbar, phase & 1);
+    phase++;
+    const bool staged = d.ncp > 0 && d.sp < 0;
+    if (staged && A.discard) {
+        const char *base = reinterpret_cast<const char *>(A.edges);
+        const size_t a = (size_t)d.src * 8, z = a + (size_t)d.cap * 8;
+        for (size_t l = (a + 127) & ~(size_t)127; l + 128 <= z; l += 128) discard_l2_line(base + l);
+    }
+    const bool even = (d.dst & 1) == 0;
+    if (staged && even) {
+        const unsigned nb = (unsigned)(d.ncp & ~1) * 8;
+        if (nb) bulk_s2g(A.out_e + d.dst, buf + d.off, nb);
+        if (d.ncp & 1) {
+            int2 e;
+            asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(buf + d.off + (unsigned)(d.ncp - 1) * 8));
+            __stcs(A.out_e + d.dst + d.ncp - 1, e);
+        }
+    }
+    bulk_commit();
+    unsigned odd = __ballot_sync(0xffffffffu, staged && !even);
+    while (odd) {
+        const int k = __ffs(odd) - 1;
+        odd &= odd - 1;
+        const long long d_k = __shfl_sync(0xffffffffu, d.dst, k);
+        const int c_k = __shfl_sync(0xffffffffu, d.ncp, k);
+        const unsigned o_k = __shfl_sync(0xffffffffu, d.off, k);
+        for (int e0 = 2 * lane; e0 < c_k + 1; e0 += 64) {
+            if (e0 == 0) {  // element 0 alone; pairs (e0 - 1, e0) after it are 16-byte aligned
+                int2 e;
+                asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(buf + o_k));
+                __stcs(A.out_e + d_k, e);
+                continue;
+            }
+            int2 x0, x1;
+            asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(x0.x), "=r"(x0.y) : "r"(buf + o_k + (unsigned)(e0 - 1) * 8));
+            if (e0 < c_k) {
+                asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(x1.x), "=r"(x1.y) : "r"(buf + o_k + (unsigned)e0 * 8));
+                __stcs(reinterpret_cast<int4 *>(A.out_e + d_k + e0 - 1), make_int4(x0.x, x0.y, x1.x, x1.y));
+            } else {
+                __stcs(A.out_e + d_k + e0 - 1, x0);
+            }
+        }
+    }
+    sub_copy_spilled(A, d, false);  // spilled tasks (slot + spill region): plain warp copy
+}
+
+// The copier warp of a fused block: resolve and copy the block's finished batches until every
+// sampler warp of the block has left and the ring is empty.  A poll costs one status load per
+// finished entry, all in parallel (lane l owns entries l and l + 32): the word of the predecessor
+// its look-back is suspended on.  Only entries whose word has become non-zero walk further.
+template <int kGather>
+__device__ __forceinline__ void copier_loop(const SampleArgs &A, BlockRing &Rg, int n_samplers, int kb, uint32_t stage)
+{
+    const int lane = threadIdx.x & 31;
+    // pipeline state: the sub-batch whose loads are in flight (finished after the next one is issued)
+    unsigned ph[2] = {0, 0};
+    const uint32_t mb[2] = {(uint32_t)__cvta_generic_to_shared(&Rg.mbar[0]),
+                            (uint32_t)__cvta_generic_to_shared(&Rg.mbar[1])};
+    SubDesc pd;
+    pd.ncp = 0;
+    bool pending = false;
+    unsigned ptot = 0;
+    int pbuf = 0, nbuf = 0;
+    auto flush = [&]() {
+        if (!pending) return;
+        if (ptot) {
+            sub_finish(A, pd, stage + (uint32_t)pbuf * kStageBuf, mb[pbuf], ph[pbuf]);
+        } else {  // nothing staged (spilled tasks only)
+            SubDesc z = pd;
+            sub_finish_nowait(A, z);
+        }
+        pending = false;
+    };
+    auto copy_batch = [&](int64_t b, int64_t prefix, int64_t agg) {
+        const int64_t T = A.n_tasks;
+        const int64_t t0 = b * kb, t1 = min(T, t0 + kb);
+        if (t1 == T && lane == 0) A.dest[T] = prefix + agg;
+        int64_t run = prefix;
+        for (int64_t tb = t0; tb < t1; tb += 32) {
+            SubDesc d;
+            const unsigned tot = sub_prep(A, tb, t1, run, d);
+            if (tot <= (unsigned)kStageBuf) {
+                const int x = nbuf;
+                // buffer x's previous stores must have read it: at most the other buffer's group pending
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncwarp();
+                if (tot) sub_issue(A, d, stage + (uint32_t)x * kStageBuf, mb[x], tot);
+                flush();
+                pd = d;
+                ptot = tot;
+                pbuf = x;
+                pending = true;
+                nbuf ^= 1;
+            } else {  // (rare) a sub-batch larger than a buffer: plain warp copy
+                flush();
+                sub_copy_plain(A, d);
+            }
+        }
+    };
+    for (;;) {
+        bool did = false;
+        bool any_entry = false;
+        for (int half = 0; half < kBRing / 32; half++) {  // (lane l: entries l, l + 32, ...)
+            const int el = half * 32 + lane;
+            const long long be = *(volatile long long *)&Rg.b[el];
+            const unsigned long long pk = *(volatile unsigned long long *)&Rg.packed[el];
+            any_entry = any_entry || be >= 0;
+            const int n_in = be >= 0 ? (int)min((int64_t)kb, A.n_tasks - (int64_t)be * kb) : 0;
+            const bool fin = be >= 0 && (int)(pk >> kPackShift) == n_in;
+            // per finished entry: one load of the predecessor it waits on (batch 0 waits on none)
+            bool go = false;
+            if (fin) {
+                if (be == 0) {
+                    go = true;
+                } else {
+                    const long long jw = Rg.lb_j[el] < -1 ? be - 1 : Rg.lb_j[el];
+                    go = (ld_status(A.grp_state + jw) & ~kGrpVal) != 0;
+                }
+            }
+            unsigned ready = __ballot_sync(0xffffffffu, go);
+#ifdef FM_FUSE_STATS
+            const unsigned blocked = __ballot_sync(0xffffffffu, fin && !go);
+            if (lane == 0) FSTAT(3, __popc(blocked));
+#else
+            (void)fin;
+#endif
+            while (ready) {
+                const int el0 = __ffs(ready) - 1;
+                const int e = half * 32 + el0;
+                ready &= ready - 1;
+                const int64_t b = __shfl_sync(0xffffffffu, be, el0);
+                const int64_t agg = (int64_t)(__shfl_sync(0xffffffffu, pk, el0) & ((1ull << kPackShift) - 1));
+                // look-back, 32 predecessors per step (one status word per lane): the nearest INC in
+                // the window ends it; an unfinished batch above it suspends it (resumed from there)
+                int64_t prefix = -1;
+                if (b == 0) {
+                    prefix = 0;
+                } else {
+                    int64_t j = Rg.lb_j[e] < -1 ? b - 1 : Rg.lb_j[e];  // highest predecessor not summed
+                    uint64_t pre = Rg.lb_j[e] < -1 ? 0 : Rg.lb_pre[e];
+                    for (;;) {
+                        const int64_t jj = j - lane;
+                        const uint64_t v = jj >= 0 ? ld_status(A.grp_state + jj) : kGrpInc;
+                        const uint64_t f = v & ~kGrpVal;
+                        const unsigned inc = __ballot_sync(0xffffffffu, f == kGrpInc);
+                        const unsigned zero = __ballot_sync(0xffffffffu, f == 0);
+                        const int li = inc ? __ffs(inc) - 1 : 32;    // nearest INC
+                        const int lz = zero ? __ffs(zero) - 1 : 32;  // nearest unfinished
+                        const int upto = min(li, lz);
+                        uint64_t part = (lane < upto || (lane == li && li < lz)) ? (v & kGrpVal) : 0;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                        pre += part;
+                        if (li < lz) {
+                            prefix = (int64_t)pre;
+                            break;
+                        }
+                        j -= upto;
+                        if (lz < 32) {  // suspended on predecessor j
+                            if (lane == 0) {
+                                Rg.lb_j[e] = j;
+                                Rg.lb_pre[e] = pre;
+                            }
+                            break;
+                        }
+                    }
+                    if (prefix >= 0 && lane == 0) st_status(A.grp_state + b, kGrpInc | (uint64_t)(prefix + agg));
+                }
+                if (prefix < 0) continue;
+                __threadfence_block();  // (acquire: the batch's slot data after its finished count)
+#ifdef FM_FUSE_STATS
+                const long long c0 = clock64();
+#endif
+#ifdef FM_FUSE_NOCOPY  // timing experiment only: the copier resolves but does not copy
+                if (false)
+#endif
+                if (kGather == 2)  // rank-out: the ids are mapped on the way (through registers)
+                    batch_copy<kGather>(A, b, prefix, agg, kb, Rg.desc);
+                else
+                    copy_batch(b, prefix, agg);
+#ifdef FM_FUSE_STATS
+                if (lane == 0) {
+                    FSTAT(0, 1);
+                    FSTAT(1, clock64() - c0);
+                }
+#endif
+                if (lane == 0) {  // free the entry: counter reset before the id, both before the free bit
+                    Rg.lb_j[e] = -2;
+                    *(volatile unsigned long long *)&Rg.packed[e] = 0;
+                    __threadfence_block();
+                    *(volatile long long *)&Rg.b[e] = -1;
+                    __threadfence_block();
+                    atomicOr(&Rg.free_mask[e >> 6], 1ull << (e & 63));
+                }
+                did = true;
+            }
+            __syncwarp();
+        }
+        if (!did) {
+            flush();  // (idle: complete the sub-batch in flight)
+            const unsigned ex = *(volatile unsigned *)&Rg.exited;
+            if (ex == (unsigned)n_samplers && !__any_sync(0xffffffffu, any_entry)) {
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // (writes complete)
+                break;
+            }
+            if (lane == 0) FSTAT(2, 1);
+            __nanosleep(500);
+        }
+    }
+}
+
 // kC independent chains (lane-chunk tasks) per thread, interleaved for instruction-level
 // parallelism (instantiated with kC = 1: two chains measured slower, their registers cost more
 // occupancy than their ILP gains).
@@ -103,34 +810,69 @@ __device__ __forceinline__ uint32_t load_logtab()
 // kOrdered: bipartite / directed output (row id, candidate id) as is (R16).
 // kCheck (FM_DEBUG_CHECKS=1): every landed candidate checks the contract p <= q (1 + 2^-50)
 // (DESIGN R13) and flags kErrBound -- the call then fails with FM_ERR_BOUND.
-template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArgs A)
+// kFuse: v3 fused write (UBCM edge lists; the launch's a.fuse): the block's last warp is a copier.
+template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck,
+          bool kFuse>
+__global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : kMinBlocks) k_sample(const __grid_constant__ SampleArgs A)
 {
+    // block size: kThreads (several blocks per SM), or one fused block per SM
+    constexpr int kT = kFuse ? kFuseThreads : kThreads;
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
     // rarely used per-chain task state lives in shared memory (registers are the occupancy limit)
-    __shared__ int64_t s_task[kThreads * kC];   // current task id, -1 none
-    __shared__ int64_t s_spill[kThreads * kC];  // its spill region: -1 none, -2 failed
+    __shared__ int64_t s_task[kT * kC];   // current task id, -1 none
+    __shared__ int64_t s_spill[kT * kC];  // its spill region: -1 none, -2 failed
     // 64-bit per-thread draw / accepted counters: the 32-bit registers below are added here at
     // every task end (a statistics call over many samples passes 2^32 per warp)
-    __shared__ unsigned long long s_ndraw[kThreads], s_nacc[kThreads];
+    __shared__ unsigned long long s_ndraw[kT / 32], s_nacc[kT / 32];  // per warp
     // UBCM: the last < 4 accepted edges of each lane's slot, so that the slot is written in whole
     // 32-byte sectors (structure of arrays: conflict-free)
-    __shared__ int2 s_eb[kModel == FM_UBCM ? 4 : 1][kThreads];
+    __shared__ int2 s_eb[kModel == FM_UBCM ? 4 : 1][kT];
     const bool buf4 = kModel == FM_UBCM && A.buf4 && !A.rerun_base && !kStats;
     // ECM: the scratch holds one 16-byte (src, dst, w, 0) record per edge, written two per sector
     // (the lane's previous record waits in shared memory); the compaction splits the records into
     // the edge and weight arrays (separate 8- and 4-byte stores wrote two partial sectors per edge)
-    __shared__ int4 s_er[kModel == FM_ECM ? kThreads : 1];
+    __shared__ int4 s_er[kModel == FM_ECM ? kT : 1];
     const bool aos = kModel == FM_ECM && A.buf4 && !A.rerun_base && !kStats;
+    // v3 fused write (UBCM edge lists): the block's last warp copies the finished batches of its
+    // sampler warps to the final list
+    static_assert(!kFuse || (kModel == FM_UBCM && !kStats), "fused write: UBCM edge lists only");
+    constexpr bool fuse = kFuse;
+    using Ring = std::conditional_t<kFuse, BlockRing, RingT<1, 16>>;
+    __shared__ Ring s_ring[1];
+    __shared__ unsigned char s_tslot[kFuse ? kT : 1];
+    Ring &R = s_ring[0];
+    if constexpr (kFuse) {
+        if (threadIdx.x < kBRing) {
+            R.b[threadIdx.x] = -1;
+            R.packed[threadIdx.x] = 0;
+            R.lb_j[threadIdx.x] = -2;
+            if (threadIdx.x < kBRing / 64) R.free_mask[threadIdx.x] = ~0ull;
+            if (threadIdx.x == 0) {
+                R.exited = 0;
+                mbar_init((uint32_t)__cvta_generic_to_shared(&R.mbar[0]), 1);
+                mbar_init((uint32_t)__cvta_generic_to_shared(&R.mbar[1]), 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+        }
+    }
     const SmemLogTab T{A.lc, load_logtab()};
+    if constexpr (kFuse) {
+        if ((threadIdx.x >> 5) == 0) {  // the block's copier warp
+            // the staging buffer: dynamic shared memory after the sampler warps' prefetch slots
+            copier_loop<kGather>(A, R, kT / 32 - 1, kBatch,
+                                 ((uint32_t)__cvta_generic_to_shared(s_dyn) + (uint32_t)(kT * kC * 64) + 127u) & ~127u);
+            return;
+        }
+    }
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t n_tasks = A.n_tasks_dev ? (int64_t)*A.n_tasks_dev : A.n_tasks;
 
     // ---- warp batch of task ids [bpos, bend); lane 0 holds the start of the next batch ----
-    unsigned long long next_batch = 0;
-    if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
+    unsigned long long next_batch = 0;  // (prefetched claim; the fused write claims at open time)
+    if (!kFuse && lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
     int64_t bpos = 0, bend = 0;
+    int cur_slot = 0;  // fused write: ring entry of the batch [bpos, bend)
     bool warp_done = false;
     // ---- per-chain task state ----
     int2 *eb[kC];  // the task's output slot (scratch, or the final list when re-running)
@@ -162,8 +904,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // draws; landed = draws - segments and accepted = edges are derived by the host (every
     // segment ends with exactly one terminal draw); statistics mode counts accepted edges
     uint32_t n_draw = 0, n_acc = 0;
-    s_ndraw[threadIdx.x] = 0;
-    s_nacc[threadIdx.x] = 0;
+    if ((threadIdx.x & 31) == 0) {
+        s_ndraw[threadIdx.x >> 5] = 0;
+        s_nacc[threadIdx.x >> 5] = 0;
+    }
     bool wsat = false, bad_bound = false;
 
     // segment g[c] of chain c's task becomes current (64/96-byte record; the record of the next
@@ -172,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     // structure of arrays: 16-byte part k of thread t's slot at (k * kThreads + t) * 16, so the
     // 8 lanes of a 16-byte shared access touch 8 consecutive 16-byte words (conflict-free)
     static_assert(kC == 1, "prefetch slot layout assumes one chain per thread");
-    constexpr int kPart = 16 * kThreads;
+    constexpr int kPart = 16 * kT;
     uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(s_dyn) + threadIdx.x * 16;
     asm volatile("mov.b32 %0, %0;" : "+r"(slot0));  // opaque: held in a register, not recomputed per use
     auto start_seg = [&](const int c, const bool prefetched) {
@@ -293,10 +1037,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                     if (!A.rerun_base && !kStats) {
                         A.counts[tk] = cnt[c];
                         A.spill_off[tk] = s_spill[ci];
+                        if (kFuse && fuse) {  // v3: the task is finished: count it in its batch
+                            const int sl = s_tslot[threadIdx.x];
+                            // the slot's edges (its last partial sector above), spill and count are
+                            // written: order them before the count the copier warp reads (CTA scope)
+                            __threadfence_block();
+                            const unsigned long long old =
+                                atomicAdd(&R.packed[sl], (1ull << kPackShift) | (unsigned long long)cnt[c]);
+                            const int64_t bb = R.b[sl];
+                            if ((int64_t)(old >> kPackShift) + 1 == min((int64_t)kBatch, n_tasks - bb * kBatch)) {
+                                // the batch's last task: publish its edge count (batch 0: its prefix)
+                                const uint64_t agg = (old & ((1ull << kPackShift) - 1)) + (uint64_t)cnt[c];
+                                st_status(A.grp_state + bb, (bb == 0 ? kGrpInc : kGrpAgg) | agg);
+                            }
+                        }
                     }
                     s_task[ci] = -1;
-                    s_ndraw[threadIdx.x] += n_draw;
-                    s_nacc[threadIdx.x] += n_acc;
+                    atomicAdd(&s_ndraw[threadIdx.x >> 5], (unsigned long long)n_draw);
+                    if (kStats) atomicAdd(&s_nacc[threadIdx.x >> 5], (unsigned long long)n_acc);
                     n_draw = n_acc = 0;
                 }
             }
@@ -305,17 +1063,63 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                 const int k = __popc(nc), rank = __popc(nc & lt);
                 const int64_t avail = bend - bpos;
                 int64_t my;
+                int myslot = 0;
                 if (k <= avail) {
                     my = bpos + rank;
                     bpos += k;
+                    myslot = cur_slot;
                 } else {
-                    const int64_t nb = (int64_t)__shfl_sync(0xffffffffu, next_batch, 0);
-                    my = rank < avail ? bpos + rank : nb + (rank - avail);
-                    bpos = nb + (k - avail);
-                    bend = nb + kBatch;
-                    if (lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
+                    int64_t nb;
+                    int ns = 0;
+                    if constexpr (kFuse) {
+                        // fused write: reserve a free entry of the block's ring first, then claim the
+                        // batch (no prefetched claims: every claimed batch is running, so a look-back
+                        // never waits on a batch that cannot start); no entry: the idle lanes wait
+                        int got = -1;
+                        long long nbl = 0;
+                        if (lane == 0) {
+                            // (start the search at this warp's own word: less contention)
+                            const int w0 = ((threadIdx.x >> 5) * (kBRing / 64)) / (kT / 32);
+                            for (int wq = 0; wq < kBRing / 64 && got < 0; wq++) {
+                                const int w = (w0 + wq) % (kBRing / 64);
+                                unsigned long long m = *(volatile unsigned long long *)&R.free_mask[w];
+                                while (m) {
+                                    const int e = __ffsll((long long)m) - 1;
+                                    const unsigned long long old = atomicAnd(&R.free_mask[w], ~(1ull << e));
+                                    if (old & (1ull << e)) {  // (its counter is already 0)
+                                        got = w * 64 + e;
+                                        break;
+                                    }
+                                    m = old & ~(1ull << e);
+                                }
+                            }
+                            if (got >= 0) {
+                                nbl = (long long)atomicAdd(A.task_counter, (unsigned long long)kBatch);
+                                if (nbl < n_tasks) *(volatile long long *)&R.b[got] = nbl / kBatch;
+                                else atomicOr(&R.free_mask[got >> 6], 1ull << (got & 63));  // the queue is empty
+                            }
+                        }
+                        ns = __shfl_sync(0xffffffffu, got, 0);
+                        nb = __shfl_sync(0xffffffffu, nbl, 0);
+                    } else {
+                        nb = (int64_t)__shfl_sync(0xffffffffu, next_batch, 0);
+                    }
+                    if (ns >= 0) {
+                        my = rank < avail ? bpos + rank : nb + (rank - avail);
+                        myslot = rank < avail ? cur_slot : ns;
+                        cur_slot = ns;
+                        bpos = nb + (k - avail);
+                        bend = nb + kBatch;
+                        if (!kFuse && lane == 0) next_batch = atomicAdd(A.task_counter, (unsigned long long)kBatch);
+                    } else {
+                        my = rank < avail ? bpos + rank : -1;
+                        myslot = cur_slot;
+                        bpos = bend;
+
+                    }
                 }
-                if (needc && !warp_done && my < n_tasks) {
+                if (needc && !warp_done && my >= 0 && my < n_tasks) {
+                    if (kFuse) s_tslot[threadIdx.x] = (unsigned char)myslot;
                     int64_t t = A.task_list ? A.task_list[my] : my;
                     if (A.il_s[0] > 0 && !A.task_list) {  // chunk-major queue -> canonical task index
                         const int kq = my < A.tm.t_split ? 0 : 1;
@@ -353,6 +1157,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         for (int c = 0; c < kC; c++) any_act = any_act || act[c];
         if (!__any_sync(0xffffffffu, any_act)) {
             if (warp_done) break;
+            if (kFuse && fuse) {  // (ring full: the copier is behind)
+                __nanosleep(256);
+            }
             continue;
         }
         }
@@ -531,7 +1338,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
                             const int2 e0 = s_eb[0][threadIdx.x], e1 = s_eb[1][threadIdx.x], e2 = s_eb[2][threadIdx.x];
                             // two 16-byte stores to one sector (one 256-bit STG.256 measured 1 % slower)
                             int4 *q = reinterpret_cast<int4 *>(eb[c] + (cnt[c] - 3));
-                            if (kGather == 2) {  // large N: evict-first, the L2 keeps the kappa gather target (-0.7 %)
+                            if (kGather == 2 && !kFuse) {  // large N: evict-first, the L2 keeps the kappa gather target (-0.7 %)
                                 __stcs(q, make_int4(e0.x, e0.y, e1.x, e1.y));
                                 __stcs(q + 1, make_int4(e2.x, e2.y, ev.x, ev.y));
                             } else {
@@ -571,7 +1378,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
     }
 #ifdef FM_TRACE
     if (lane == 0 && !A.rerun_base) {
-        const int wi = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        const int wi = blockIdx.x * (kT / 32) + (threadIdx.x >> 5);
         if (wi < 4096) {
             g_trace[wi][0] = tr_t0;
             g_trace[wi][1] = tr_done;
@@ -582,14 +1389,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_sample(const SampleArg
         }
     }
 #endif
+    if (kFuse && fuse) {  // after the warp's last task end
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) atomicAdd(&R.exited, 1u);
+    }
     if (kCheck && __any_sync(0xffffffffu, bad_bound) && lane == 0) atomicOr(A.flags, kErrBound);
     if (A.rerun_base) return;
-    unsigned long long dr = s_ndraw[threadIdx.x] + n_draw, ac = s_nacc[threadIdx.x] + n_acc;
+    unsigned long long dr = n_draw, ac = n_acc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         dr += __shfl_xor_sync(0xffffffffu, dr, o);
         ac += __shfl_xor_sync(0xffffffffu, ac, o);
     }
+    __syncwarp();
+    dr += s_ndraw[threadIdx.x >> 5];
+    ac += s_nacc[threadIdx.x >> 5];
     const bool anysat = __any_sync(0xffffffffu, wsat);
     if (lane == 0) {
         atomicAdd(&A.counters[0], dr);
@@ -810,6 +1625,19 @@ void dump_trace()
 }
 #endif
 
+void fuse_stats_dump()
+{
+#ifdef FM_FUSE_STATS
+    unsigned long long h[8];
+    if (cudaMemcpyFromSymbol(h, g_fstats, sizeof(h)) != cudaSuccess) return;
+    fprintf(stderr, "[fuse] copies %llu copy_cycles/copy %.0f idle_polls %llu blocked_entries %llu ring_full %llu "
+                    "all_idle_iters %llu desc_cycles/copy %.0f job_cycles/copy %.0f\n", h[0], h[0] ? (double)h[1] / h[0] : 0.0,
+            h[2], h[3], h[4], h[5], h[0] ? (double)h[6] / h[0] : 0.0, h[0] ? (double)h[7] / h[0] : 0.0);
+    static unsigned long long z[8];
+    cudaMemcpyToSymbol(g_fstats, z, sizeof(z));
+#endif
+}
+
 cudaError_t ensure_log_table(cudaStream_t st)
 {
     (void)st;
@@ -826,15 +1654,17 @@ cudaError_t ensure_log_table(cudaStream_t st)
 
 // one instantiation per (model, statistics mode, ECM bound refresh, UBCM gather record, output
 // orientation); kMinB = 3 blocks per SM
-template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck>
+template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck,
+          bool kFuse>
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
-    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kGather, kOrdered, kCheck>;
+    auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kGather, kOrdered, kCheck, kFuse>;
+    constexpr int kT = kFuse ? kFuseThreads : kThreads;
     int dev = 0, sms = 0, per = 0;
     cudaError_t err = cudaGetDevice(&dev);
     if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (err != cudaSuccess) return err;
-    const size_t dyn = (size_t)kThreads * kC * (kModel == FM_ECM ? 96 : 64);
+    const size_t dyn = (size_t)kT * kC * (kModel == FM_ECM ? 96 : 64) + (kFuse ? 2 * kStageBuf + 128 : 0);
     // function attributes are per device: set once per (instantiation, device), thread-safe
     static std::mutex attr_mu;
     static bool attr_set[kMaxDevices] = {};
@@ -852,7 +1682,7 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         int carve = cv && *cv ? atoi(cv) : 40;
         cudaFuncAttributes fa;
         if (carve >= 0 && cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
-            const size_t need = (size_t)kMinB * (fa.sharedSizeBytes + dyn + 1024);
+            const size_t need = (size_t)(kFuse ? 1 : kMinB) * (fa.sharedSizeBytes + dyn + 1024);
             const int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
             carve = std::max(carve, std::min(pct, 100));
         }
@@ -862,13 +1692,13 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         }
         attr_set[dev] = true;
     }
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kThreads, dyn);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kT, dyn);
     if (err != cudaSuccess) return err;
     int64_t blocks = (int64_t)sms * (per > 0 ? per : 1);
-    const int64_t need = (a.n_tasks + kThreads * kC - 1) / (kThreads * kC);  // <= one task per chain at start
+    const int64_t need = (a.n_tasks + kT * kC - 1) / (kT * kC);  // <= one task per chain at start
     if (need < blocks) blocks = need;
     count_launch();
-    kern<<<(unsigned)blocks, kThreads, dyn, st>>>(a);
+    kern<<<(unsigned)blocks, kT, dyn, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -880,8 +1710,11 @@ static cudaError_t launch_sample_c(const SampleArgs &a, cudaStream_t st)
     // statistics mode writes no pairs: its orientation is irrelevant
     if constexpr (!kStats)
         if (kGather != 2 && a.ordered)
-            return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, true, kCheck>(a, st);
-    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, false, kCheck>(a, st);
+            return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, true, kCheck, false>(a, st);
+    if constexpr (kModel == FM_UBCM && !kStats)
+        if (a.fuse && !a.rerun_base && !a.ordered)
+            return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, false, kCheck, true>(a, st);
+    return launch_sample_t<kModel, kMinB, 1, kStats, kRefresh, kGather, false, kCheck, false>(a, st);
 }
 
 template <int kModel, bool kStats, bool kRefresh, int kGather>

@@ -220,3 +220,20 @@ def test_status_codes():
     with pytest.raises(fm.FastMaxEntError) as ex:
         fm.sample_ubcm(p, 1, 2, first_sample=2**32 - 1)
     assert ex.value.status == fm.FM_ERR_INVALID
+
+
+# ------------------------------------------------------------------------------ v3 fused write
+@pytest.mark.parametrize("n,S,R", [(1000, 8, 20), (20_011, 64, 3), (100_000, 256, 7)])
+def test_fused_write_option_parity(O, n, S, R):
+    """FM_FUSE_WRITE=1 (opt-in v3 write path): the same lists as the default path
+    and the oracle, element by element."""
+    x, _ = WL.random_fitness(11 * n + 5, n, 2.4, 0.03 if n < 50_000 else 0.005)
+    os.environ["FM_FUSE_WRITE"] = "1"
+    try:
+        plan, e, E, _ = gpu_run(x, None, S, 4242, R, first_sample=1)
+    finally:
+        os.environ.pop("FM_FUSE_WRITE", None)
+    _, e0, E0, _ = gpu_run(x, None, S, 4242, R, first_sample=1)
+    assert np.array_equal(e.offsets, e0.offsets) and np.array_equal(E, E0)
+    ref = O.sample(O.sort_plan(x, seg_target=S), 4242, n_samples=R, first_sample=1, nthreads=O.ncores())
+    assert np.array_equal(E, ref.edges)
