@@ -16,7 +16,8 @@
  *    fm_last_error() returns a thread-local message.
  *  - Device temporaries come from the device's default stream-ordered memory pool, whose release
  *    threshold the library bounds at the first call on a device (FM_POOL_RELEASE_BYTES, default
- *    1/4 of the device memory): freed memory above it is returned to the device.
+ *    3/4 of the device memory): freed memory above it is returned to the device; fm_pool_trim()
+ *    returns the cached memory on demand.
  *  - All work is ordered on the caller's CUDA stream `cuda_stream` (cudaStream_t; NULL = the
  *    legacy default stream) on the current device.
  *  - Input pointers may be HOST or DEVICE memory (detected with cudaPointerGetAttributes); they
@@ -222,6 +223,10 @@ fm_status fm_timing_get(fm_timing *t, int reset);
  * by the sampler's Markstein division (in holds 2n doubles; must equal the IEEE quotient).
  * Stream-ordered. */
 fm_status fm_debug_eval(int32_t fn, int64_t n, const double *in_dev, double *out_dev, void *cuda_stream);
+
+/* Release the memory the current device's default pool holds cached beyond keep_bytes (freed
+ * temporaries of earlier calls) back to the device.  Synchronises the device. */
+fm_status fm_pool_trim(uint64_t keep_bytes);
 
 /* Release an fm_plan* or the buffers of an fm_edges* (the struct itself is caller-owned and
  * is zeroed).  Objects are tagged; NULL is a no-op. */

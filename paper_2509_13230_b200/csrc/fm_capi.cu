@@ -118,10 +118,11 @@ struct Allocs {
 };
 
 // The stream-ordered temporaries of a call (scratch ~1.3x the edge list) come from the device's
-// default pool.  Its release threshold is bounded (FM_POOL_RELEASE_BYTES, default 1/4 of the
+// default pool.  Its release threshold is bounded (FM_POOL_RELEASE_BYTES, default 3/4 of the
 // device memory): memory freed by a call stays mapped for the next call up to that size (no
-// remapping per call), and anything above it is returned to the device at the next
-// synchronisation, so a large call does not starve other allocators (PyTorch's) afterwards.
+// remapping per call: at 1/4 the 35-50 GB working set of a config-5 call was released and
+// re-mapped at every plan's synchronisation, 1-14 ms of jitter), and anything above it is returned
+// to the device at the next synchronisation; fm_pool_trim() releases the cached memory on demand.
 void configure_pool(int dev)
 {
     static std::mutex mu;
@@ -134,7 +135,7 @@ void configure_pool(int dev)
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) total = prop.totalGlobalMem;
         const char *v = getenv("FM_POOL_RELEASE_BYTES");
-        uint64_t thr = v && *v ? strtoull(v, nullptr, 10) : (uint64_t)(total / 4);
+        uint64_t thr = v && *v ? strtoull(v, nullptr, 10) : (uint64_t)(total / 4 * 3);
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
@@ -719,6 +720,7 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             r.weights = (int32_t *)own->weights;
             return launch_sample(model, r, st);
         };
+        unsigned int plan_flags = 0;
         // one pass of the call: sampler (+ copiers), offsets, overflow list; the host learns the total
         // at the one synchronisation
         auto run_pass = [&](int64_t cap) -> fm_status {
@@ -748,13 +750,14 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
                "read offsets");
             CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+            // (pageable destinations: these reads are the call's synchronisation; the plan's flag word
+            // is read here too, after every launch, not before the sampler)
+            CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
+               "read plan flags");
             tw.end(st);
             CK(cudaStreamSynchronize(st), "sync (sample)");
             return FM_OK;
         };
-        unsigned int plan_flags = 0;
-        CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
-           "read plan flags");
         {
             fm_status r = run_pass(out_cap);
             if (r != FM_OK) return r;
@@ -1090,6 +1093,17 @@ fm_status fm_debug_eval(int32_t fn, int64_t n, const double *in_dev, double *out
 {
     if (fn < 0 || fn > 3 || n < 0 || (n > 0 && (!in_dev || !out_dev))) return fail(FM_ERR_INVALID, "bad debug_eval args");
     CK(launch_debug_eval(fn, n, in_dev, out_dev, (cudaStream_t)cuda_stream), "debug eval");
+    return FM_OK;
+}
+
+fm_status fm_pool_trim(uint64_t keep_bytes)
+{
+    int dev = 0;
+    CK(cudaGetDevice(&dev), "cudaGetDevice");
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev), "default pool");
+    CK(cudaDeviceSynchronize(), "sync");
+    CK(cudaMemPoolTrimTo(pool, (size_t)keep_bytes), "trim");
     return FM_OK;
 }
 

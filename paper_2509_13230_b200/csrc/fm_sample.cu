@@ -1053,9 +1053,11 @@ __global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : k
                         }
                     }
                     s_task[ci] = -1;
+#ifndef FM_THREAD_COUNTERS
                     atomicAdd(&s_ndraw[threadIdx.x >> 5], (unsigned long long)n_draw);
                     if (kStats) atomicAdd(&s_nacc[threadIdx.x >> 5], (unsigned long long)n_acc);
                     n_draw = n_acc = 0;
+#endif
                 }
             }
             const uint32_t nc = __ballot_sync(0xffffffffu, needc && !warp_done);

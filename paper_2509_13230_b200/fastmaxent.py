@@ -30,7 +30,8 @@ STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ER
 FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
 _KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
 SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_sample_ecm_ex", "fm_edges_to_host", "fm_plan_get_info",
-           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval", "fm_expected_degrees"]
+           "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval", "fm_expected_degrees",
+           "fm_pool_trim"]
 
 
 class FastMaxEntError(RuntimeError):
@@ -81,8 +82,12 @@ def _load():
     L.fm_sample_degrees.restype = C.c_int
     L.fm_sample_richclub.argtypes = [vp, u64, i64, i64, vp, vp, C.POINTER(_Counters)]
     L.fm_sample_richclub.restype = C.c_int
-    L.fm_expected_degrees.argtypes = [C.c_int, i64, vp, vp, vp, i64, vp, vp, vp, vp, vp]
-    L.fm_expected_degrees.restype = C.c_int
+    if hasattr(L, "fm_expected_degrees") or not os.environ.get("FM_LIB_VARIANT"):  # (older A/B builds lack it)
+        L.fm_expected_degrees.argtypes = [C.c_int, i64, vp, vp, vp, i64, vp, vp, vp, vp, vp]
+        L.fm_expected_degrees.restype = C.c_int
+    if hasattr(L, "fm_pool_trim") or not os.environ.get("FM_LIB_VARIANT"):
+        L.fm_pool_trim.argtypes = [u64]
+        L.fm_pool_trim.restype = C.c_int
     L.fm_edges_to_host.argtypes = [C.POINTER(_Edges), vp, vp, vp]
     L.fm_edges_to_host.restype = C.c_int
     L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
@@ -384,6 +389,11 @@ def expected_degrees(x, y=None, nodes=None, stream=None):
     _check(lib.fm_expected_degrees(FM_UBCM if y is None else FM_ECM, n, px, py, pn, m, *ptr, _stream(stream)))
     del kx, ky, keep_nodes
     return (out[0], out[1], None, None) if y is None else tuple(out)
+
+
+def pool_trim(keep_bytes: int = 0) -> None:
+    """fm_pool_trim: return the device pool's cached temporaries beyond keep_bytes to the device."""
+    _check(lib.fm_pool_trim(int(keep_bytes)))
 
 
 def abi_version() -> int:
