@@ -44,6 +44,12 @@ std::vector<Pending> g_pending;
 std::atomic<bool> g_timing{false};
 double g_phase_ms[3] = {0, 0, 0};
 long long g_sample_launches = 0;
+// a sample call's spans: a .. b = first sampler start to last sampler end (the pipelined groups'
+// samplers overlap each other and the preceding groups' compactions), b .. c = the exposed rest
+struct CallSpan {
+    cudaEvent_t a, b, c;
+};
+std::vector<CallSpan> g_call_spans;
 
 struct PhaseTimer {
     int phase = -1;
@@ -142,6 +148,25 @@ void configure_pool(int dev)
     done[dev] = true;
 }
 
+// one non-blocking side stream per device for the pipelined sample groups (shared by concurrent
+// calls: they are ordered by events, sharing only costs overlap)
+cudaError_t side_stream(cudaStream_t *out)
+{
+    static std::mutex mu;
+    static cudaStream_t side[kMaxDevices] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!side[dev]) {
+        e = cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+    }
+    *out = side[dev];
+    return cudaSuccess;
+}
+
 bool is_device_ptr(const void *p)
 {
     cudaPointerAttributes a;
@@ -185,7 +210,7 @@ void plan_release(Plan *p)
     cudaFree(p->ymax);
     cudaFree(p->ly_s);
     cudaFree(p->rec);
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < 3; k++) {
         cudaFree(p->chunk_seg[k]);
         cudaFree(p->chunk_cap[k]);
     }
@@ -451,14 +476,20 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
         CK(scan_exclusive_i64(seg_work, seg_work, n_seg, work2, wb, st), "scan work");
     }
 
-    // ---- lane-chunking (never changes results): coarse and fine ----
+    // ---- lane-chunking (never changes results): coarse, fine and big (FM_CHUNK_BIG_DRAWS=0: none) ----
     const int64_t total = h_sc.total_work;
-    const int64_t lane_draws[2] = {std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128)),
-                                   std::max<int64_t>(1, env_i64("FM_CHUNK_FINE_DRAWS", 64))};
+    const int64_t lane_draws[3] = {std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128)),
+                                   std::max<int64_t>(1, env_i64("FM_CHUNK_FINE_DRAWS", 64)),
+                                   std::max<int64_t>(0, env_i64("FM_CHUNK_BIG_DRAWS", 512))};
     const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
     p->slots_aligned = true;
     p->cap_per_sample = 0;
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < 3; k++) {
+        if (lane_draws[k] == 0) {  // (no big chunking)
+            p->n_chunks[k] = 0;
+            p->chunk_target[k] = 0;
+            continue;
+        }
         const int64_t target = lane_draws[k] * kUnit;
         p->chunk_target[k] = target;
         const int64_t nch = std::max<int64_t>(1, (total + target - 1) / target);
@@ -518,29 +549,51 @@ fm_status fm_sort_plan_bipartite(fm_model model, fm_graph kind, int64_t n_plus, 
                           plan_out);
 }
 
-// task space of a call: the last K samples use the fine chunks, K covering ~FM_TAIL_FACTOR times
-// the work the resident lanes hold in coarse tasks (so the end of the queue is short tasks)
-static TaskMap make_task_map(const Plan *p, int64_t n_samples, int64_t *n_tasks)
+// task space of a sample group of n_samples: its last K_fine samples use the fine chunks, the K_mid
+// before them the coarse ones, the rest (the bulk of a large call) the big ones.  The call's last
+// group: K_fine covers ~FM_TAIL_FACTOR times the work the resident lanes hold in coarse tasks (so
+// the end of the queue is short tasks), K_mid likewise for big tasks.
+static TaskMap make_task_map(const Plan *p, int64_t n_samples, int64_t K_fine, int64_t K_mid, int64_t *n_tasks)
 {
     TaskMap tm;
-    for (int k = 0; k < 2; k++) {
-        tm.seg[k] = p->chunk_seg[k];
-        tm.cap[k] = p->chunk_cap[k];
-        tm.n_chunks[k] = p->n_chunks[k];
-        tm.inv_chunks[k] = p->n_chunks[k] > 0 ? 1.0 / (double)p->n_chunks[k] : 0.0;
+    const int plan_k[kRanges] = {2, 0, 1};  // range -> the plan's chunking (big, coarse, fine)
+    for (int r = 0; r < kRanges; r++) {
+        const int k = plan_k[r];
+        tm.seg[r] = p->chunk_seg[k];
+        tm.cap[r] = p->chunk_cap[k];
+        tm.n_chunks[r] = p->n_chunks[k];
+        tm.inv_chunks[r] = p->n_chunks[k] > 0 ? 1.0 / (double)p->n_chunks[k] : 0.0;
     }
     tm.cap_per_sample = p->cap_per_sample;
+    K_fine = std::max<int64_t>(0, std::min(K_fine, n_samples));
+    K_mid = std::max<int64_t>(0, std::min(K_mid, n_samples - K_fine));
+    if (p->n_chunks[2] == 0) K_mid = n_samples - K_fine;  // no big chunking
+    const int64_t n_big = n_samples - K_fine - K_mid;
+    tm.s0[0] = 0;
+    tm.s0[1] = n_big;
+    tm.s0[2] = n_big + K_mid;
+    tm.t0[0] = 0;
+    tm.t0[1] = n_big * tm.n_chunks[0];
+    tm.t0[2] = tm.t0[1] + K_mid * tm.n_chunks[1];
+    *n_tasks = tm.t0[2] + K_fine * tm.n_chunks[2];
+    return tm;
+}
+
+// samples at the end of a call that do not use the chunking `k` of the plan (0 coarse: they use
+// the fine chunks; 2 big: they use the coarse or fine ones): ~FM_TAIL_FACTOR times the work the
+// resident lanes hold in tasks of that chunking
+static int64_t tail_samples(const Plan *p, int k)
+{
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const double lanes = (double)sms * 768.0;
-    const double tail = (double)env_i64("FM_TAIL_FACTOR", 2) * lanes * (double)(p->chunk_target[0] >> kG);
+    // (big tasks: a warp claims 64 queue entries at a time, two long tasks per lane, so the work
+    // behind the big range must be larger: with factor 2 configs 3 and 4 lost 5-14 %)
+    const int64_t factor = k == 2 ? env_i64("FM_TAIL_FACTOR_BIG", 4) : env_i64("FM_TAIL_FACTOR", 2);
+    const double tail = (double)factor * lanes * (double)(p->chunk_target[k] >> kG);
     const double per = std::max<double>(1.0, (double)p->est_draws);
-    const int64_t K = std::min<int64_t>(n_samples, (int64_t)std::ceil(tail / per));
-    tm.s_split = n_samples - K;
-    tm.t_split = tm.s_split * tm.n_chunks[0];
-    *n_tasks = tm.t_split + K * tm.n_chunks[1];
-    return tm;
+    return (int64_t)std::ceil(tail / per);
 }
 
 
@@ -580,8 +633,16 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     } og{own};
     if (!offsets_h) return fail(FM_ERR_NOMEM, "host offsets");
 
-    int64_t n_tasks = 0;
-    const TaskMap tm = make_task_map(p, n_samples, &n_tasks);
+    // ---- the call = G SAMPLE GROUPS, pipelined ----
+    // Group g (consecutive samples) runs sampler -> count scan -> offsets -> overflow list ->
+    // compaction on stream g & 1 (the caller's stream and one side stream): while the persistent
+    // sampler of group g + 1 fills the GPU, the small-footprint compaction of group g runs next to
+    // it on every SM (HBM is ~10 % busy under the sampler), and the sampler blocks of group g + 1
+    // take over the SMs as the blocks of group g run out of tasks (no end-of-launch tail between
+    // groups).  Only the last group's compaction is exposed.  Scratch slots are double-buffered
+    // over the groups (2/G of the per-call scratch).  The groups' edges are consecutive in the
+    // final list: group g's base is the device-side running total gbase[g].  Results do not depend
+    // on G.  One host synchronisation at the end of the call.
     struct Hdr {
         unsigned long long counters[3];
         unsigned int flags;
@@ -590,86 +651,110 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         unsigned long long task_counter;
         unsigned long long spill_counter;
     };
-    Hdr h;
-    memset(&h, 0, sizeof(h));
-    if (n_tasks > 0) {
-        int2 *se;
-        int32_t *sw = nullptr;
-        int64_t *counts, *dest, *ovl, *offs_d, *spill_off;
-        Hdr *hd;
-        const int64_t slots = n_samples * p->cap_per_sample;
-        const int64_t spill_cap = slots / 32 + 65536;
-        // ECM with aligned slots: 16-byte (src, dst, w, 0) records in the slots (two int2 words per
-        // edge); the spill area keeps separate edge / weight arrays
-        const bool ecm_rec = model == FM_ECM && p->slots_aligned && env_i64("FM_SCRATCH_BUF4", 1) != 0;
-        const int64_t slot_words = ecm_rec ? 2 * slots : slots, wslots = ecm_rec ? 0 : slots;
-        CK(tmp.get(&se, slot_words + spill_cap), "alloc scratch edges");
-        if (model == FM_ECM) CK(tmp.get(&sw, wslots + spill_cap), "alloc scratch weights");
-        CK(tmp.get(&spill_off, n_tasks), "alloc spill offsets");
-        CK(tmp.get(&counts, n_tasks + 1), "alloc counts");
-        CK(tmp.get(&dest, n_tasks + 1), "alloc dest");
-        CK(tmp.get(&ovl, n_tasks), "alloc overflow list");
-        CK(tmp.get(&offs_d, n_samples + 1), "alloc offsets");
-        CK(tmp.get(&hd, 1), "alloc hdr");
-        const size_t stb = scan_tmp_bytes(n_tasks + 1);
-        char *scan_tmp;
-        CK(tmp.get(&scan_tmp, stb), "alloc scan tmp");
-        CK(cudaMemsetAsync(hd, 0, sizeof(Hdr), st), "memset hdr");
-
+    struct Group {
+        int64_t s0 = 0, R = 0, n_tasks = 0;
+        TaskMap tm;
+        int64_t *counts = nullptr, *dest = nullptr, *spill_off = nullptr, *ovl = nullptr;
         SampleArgs a;
-        memset(&a, 0, sizeof(a));
-        a.rec = p->rec;
-        a.kappa_s = p->ckappa;  // candidates (R16): the - set, or the rows themselves
-        a.y_s = p->cy;
-        a.ly_s = p->cly;
-        a.perm = p->cperm;
-        a.cand = p->cand;
-        a.ymax_c = (model == FM_ECM && (flags & FM_SAMPLE_BETA_REFRESH)) ? p->ymax : nullptr;
-        a.ordered = p->kind != FM_UNDIRECTED;
-        a.buf4 = p->slots_aligned && env_i64("FM_SCRATCH_BUF4", 1) != 0;
-        // UBCM with a large candidate set (the kappa array no longer L2-resident): the sampler
-        // gathers kappa only and the compaction maps candidate ranks to ids (sampler kernel
-        // -14 %, compaction +0.55 ms on config 4: a net gain; at N <= 1e6 the compaction's extra
-        // gathers cost more than the sampler saves)
-        a.rank_out = model == FM_UBCM && p->nc >= env_i64("FM_UBCM_RANK_OUT_MIN", int64_t(1) << 21);
-        // large candidate sets (configs 4, 5): the samples of a lane-chunk run back to back, so its
-        // segment records come from DRAM once per launch instead of once per sample (sampler
-        // -2.2 % on config 4, -1.9 % on config 5; +1 % (UBCM) / +2.6 % (ECM) at N = 1e5, where
-        // the records stay in L2 anyway: off there).  Results do not depend on it.
-        // v3 fused write (UBCM, opt-in FM_FUSE_WRITE=1): one block per SM whose warp 0
-        // copies the block's finished task batches into the final list (TMA bulk copies through shared
-        // memory, decoupled look-back offsets, L2 discard of the scratch) while 23 warps sample.  Measured
-        // at parity with the separate compaction, not faster (the copier warp is issue-starved next to
-        // 23 sampler warps; the sampler loses a warp), so the default stays the compaction pass.
-        const bool fuse = model == FM_UBCM && p->slots_aligned && env_i64("FM_FUSE_WRITE", 0) != 0 &&
-                          (!a.rank_out || env_i64("FM_FUSE_RANKOUT", 0) != 0);
-        a.il_s[0] = a.il_s[1] = 0;
-        // (the fused copy needs batches of consecutive canonical tasks: sample-major queue)
-        if (!fuse && p->nc >= env_i64("FM_INTERLEAVE_MIN", int64_t(1) << 19)) {
-            a.il_s[0] = tm.s_split;
-            a.il_s[1] = n_samples - tm.s_split;
-            if (a.il_s[0] == 0) a.il_s[0] = 1;  // range 0 empty: never indexed
-            if (a.il_s[1] == 0) a.il_s[1] = 1;
+    };
+    const bool ecm_rec = model == FM_ECM && p->slots_aligned && env_i64("FM_SCRATCH_BUF4", 1) != 0;
+    const bool buf4 = p->slots_aligned && env_i64("FM_SCRATCH_BUF4", 1) != 0;
+    // v3 fused write (UBCM, opt-in FM_FUSE_WRITE=1): one block per SM whose warp 0
+    // copies the block's finished task batches into the final list.  Measured slower than the
+    // compaction pass (the copier warp is issue-starved next to 23 sampler warps); one group only.
+    const bool rank_out = model == FM_UBCM && p->nc >= env_i64("FM_UBCM_RANK_OUT_MIN", int64_t(1) << 21);
+    const bool fuse = model == FM_UBCM && p->slots_aligned && env_i64("FM_FUSE_WRITE", 0) != 0 &&
+                      (!rank_out || env_i64("FM_FUSE_RANKOUT", 0) != 0);
+    // the small-footprint compaction needs 32-byte-aligned slots holding pairs (UBCM) or records
+    // (ECM) and a warp's 32 tasks spanning < 2^31 output positions (slot <= ~1.25 (chunk + segment))
+    const bool small_compact = buf4 && (model == FM_UBCM || ecm_rec) && (p->wmax >> kG) < (int64_t(1) << 22) &&
+                               env_i64("FM_COMPACT_SMALL", 1) != 0;
+    // group count: FM_SAMPLE_GROUPS (default 1).  Measured on the B200: the
+    // co-resident compaction does hide under the next group's sampler, but every extra sampler
+    // launch pays its own end-of-launch tail (~0.4 ms on config 5: a block stays resident until its
+    // slowest lane ends, so the next group's blocks cannot move in early) and the sampler loses the
+    // issue slots the compaction takes (+7 % per co-run group), so one group is the fastest on all
+    // five configs; the option stays for memory-bound callers (scratch is 2/G of the call's).
+    int64_t G = 1;
+    if (n_samples > 1 && small_compact && !fuse) {
+        const int64_t forced = env_i64("FM_SAMPLE_GROUPS", 1);
+        if (forced > 0) G = forced;
+        G = std::min<int64_t>(G, n_samples);
+    }
+    // samples of the last K use the fine chunks (short end-of-queue tasks): the call's last group only
+    const int64_t K_fine = tail_samples(p, 0), K_big_tail = p->n_chunks[2] > 0 ? tail_samples(p, 2) : 0;
+    std::vector<Group> grp((size_t)G);
+    int64_t n_tasks = 0, max_R = 0, max_tasks = 0;
+    for (int64_t g = 0; g < G; g++) {
+        Group &q = grp[(size_t)g];
+        q.s0 = n_samples * g / G;
+        q.R = n_samples * (g + 1) / G - q.s0;
+        // (the call's last group ends with coarse, then fine tasks; the groups before it run into
+        // their successors, no tail to shorten)
+        const int64_t kf = g == G - 1 ? std::min(K_fine, q.R) : 0;
+        const int64_t km = g == G - 1 ? std::max<int64_t>(0, std::min(K_big_tail, q.R) - kf) : 0;
+        q.tm = make_task_map(p, q.R, kf, km, &q.n_tasks);
+        n_tasks += q.n_tasks;
+        max_R = std::max(max_R, q.R);
+        max_tasks = std::max(max_tasks, q.n_tasks);
+    }
+    std::vector<Hdr> h((size_t)G);
+    std::vector<int64_t> gbase_h((size_t)G + 1, 0);
+    memset(h.data(), 0, sizeof(Hdr) * (size_t)G);
+    if (n_tasks > 0) {
+        // ---- streams: groups alternate between the caller's stream and the device's side stream ----
+        cudaStream_t side = st;
+        std::vector<cudaEvent_t> evs;
+        struct EvGuard {
+            std::vector<cudaEvent_t> &v;
+            ~EvGuard()
+            {
+                for (cudaEvent_t e : v)
+                    if (e) cudaEventDestroy(e);
+            }
+        } evg{evs};
+        auto new_event = [&](cudaEvent_t *e, bool timing) -> cudaError_t {
+            cudaError_t r = cudaEventCreateWithFlags(e, timing ? cudaEventDefault : cudaEventDisableTiming);
+            if (r == cudaSuccess) evs.push_back(*e);
+            return r;
+        };
+        if (G > 1) CK(side_stream(&side), "side stream");
+        auto stream_of = [&](int64_t g) { return (g & 1) ? side : st; };
+
+        // ---- device memory (all from the caller's stream, before the fork) ----
+        const int64_t slots = max_R * p->cap_per_sample;
+        const int64_t spill_cap = slots / 32 + 65536;
+        const int64_t slot_words = ecm_rec ? 2 * slots : slots, wslots = ecm_rec ? 0 : slots;
+        const int nbuf = G > 1 ? 2 : 1;
+        int2 *se[2] = {nullptr, nullptr};
+        int32_t *sw[2] = {nullptr, nullptr};
+        // (look-back words of every group's count scan: one array, cleared once per pass)
+        const size_t stb = (scan_tmp_bytes(max_tasks + 1) + 255) & ~(size_t)255;
+        char *scan_tmp;
+        CK(tmp.get(&scan_tmp, stb * (size_t)G), "alloc scan tmp");
+        for (int b = 0; b < nbuf; b++) {
+            CK(tmp.get(&se[b], slot_words + spill_cap), "alloc scratch edges");
+            if (model == FM_ECM) CK(tmp.get(&sw[b], wslots + spill_cap), "alloc scratch weights");
         }
-        a.tm = tm;
-        a.key = philox_key(seed);
-        a.lc = log_consts();
-        a.first_sample = (uint32_t)first_sample;
-        a.n_tasks = n_tasks;
-        a.task_counter = &hd->task_counter;
-        a.edges = se;
-        a.weights = sw;
-        a.counts = counts;
-        a.spill_e = se + slot_words;
-        a.spill_w = sw ? sw + wslots : nullptr;
-        a.spill_counter = &hd->spill_counter;
-        a.spill_cap = spill_cap;
-        a.spill_off = spill_off;
-        a.counters = hd->counters;
-        a.flags = &hd->flags;
-        a.check = env_i64("FM_DEBUG_CHECKS", 0) != 0;
+        Hdr *hd;
+        int64_t *offs_d, *gbase;
+        CK(tmp.get(&hd, (size_t)G), "alloc hdr");
+        CK(tmp.get(&offs_d, n_samples + 1), "alloc offsets");
+        CK(tmp.get(&gbase, (size_t)G + 1), "alloc group bases");
+        for (int64_t g = 0; g < G; g++) {
+            Group &q = grp[(size_t)g];
+            CK(tmp.get(&q.spill_off, q.n_tasks), "alloc spill offsets");
+            CK(tmp.get(&q.counts, q.n_tasks + 1), "alloc counts");
+            CK(tmp.get(&q.dest, q.n_tasks + 1), "alloc dest");
+            CK(tmp.get(&q.ovl, q.n_tasks), "alloc overflow list");
+        }
+        // fused-write bookkeeping: one look-back status word per queue batch of kQueueBatch tasks
+        const int64_t n_batches = (n_tasks + kQueueBatch - 1) / kQueueBatch;
+        unsigned long long *grp_state = nullptr;
+        if (fuse) CK(tmp.get(&grp_state, n_batches), "alloc batch states");
+
         // capacity of the final list: the plan's hint (see the end of this block), at most the scratch's
-        int64_t out_cap = slots + spill_cap;
+        int64_t out_cap = n_samples * p->cap_per_sample + (n_samples * p->cap_per_sample / 32 + 65536);
         {
             double ratio;
             {
@@ -691,71 +776,206 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             if (own->weights) cudaFreeAsync(own->weights, st);
             own->edges = own->weights = nullptr;
         };
-        // fused-write bookkeeping: one look-back status word per queue batch of kQueueBatch tasks
-        const int64_t n_groups = (n_tasks + kQueueBatch - 1) / kQueueBatch;
-        unsigned long long *grp_state = nullptr;
-        if (fuse) {
-            CK(tmp.get(&grp_state, n_groups), "alloc batch states");
-            a.fuse = 1;
-            a.n_groups = n_groups;
-            a.grp_state = grp_state;
-            a.dest = dest;
-            a.discard = env_i64("FM_DISCARD", 1) != 0;
-            a.rank_map = a.rank_out ? p->cperm : nullptr;
+
+        // ---- per-group sampler arguments ----
+        for (int64_t g = 0; g < G; g++) {
+            Group &q = grp[(size_t)g];
+            const int b = nbuf == 2 ? (int)(g & 1) : 0;
+            SampleArgs &a = q.a;
+            memset(&a, 0, sizeof(a));
+            a.rec = p->rec;
+            a.kappa_s = p->ckappa;  // candidates (R16): the - set, or the rows themselves
+            a.y_s = p->cy;
+            a.ly_s = p->cly;
+            a.perm = p->cperm;
+            a.cand = p->cand;
+            a.ymax_c = (model == FM_ECM && (flags & FM_SAMPLE_BETA_REFRESH)) ? p->ymax : nullptr;
+            a.ordered = p->kind != FM_UNDIRECTED;
+            a.buf4 = buf4;
+            // UBCM with a large candidate set (the kappa array no longer L2-resident): the sampler
+            // gathers kappa only and the compaction maps candidate ranks to ids (sampler kernel
+            // -14 %, compaction +0.55 ms on config 4: a net gain; at N <= 1e6 the compaction's extra
+            // gathers cost more than the sampler saves)
+            a.rank_out = rank_out;
+            // large candidate sets (configs 4, 5): the samples of a lane-chunk run back to back, so its
+            // segment records come from DRAM once per launch instead of once per sample (sampler
+            // -2.2 % on config 4, -1.9 % on config 5; +1 % (UBCM) / +2.6 % (ECM) at N = 1e5, where
+            // the records stay in L2 anyway: off there).  Results do not depend on it.
+            // (the fused copy needs batches of consecutive canonical tasks: sample-major queue)
+            a.il_s[0] = a.il_s[1] = a.il_s[2] = 0;
+            if (!fuse && p->nc >= env_i64("FM_INTERLEAVE_MIN", int64_t(1) << 19)) {
+                for (int r = 0; r < kRanges; r++) {
+                    a.il_s[r] = (r + 1 < kRanges ? q.tm.s0[r + 1] : q.R) - q.tm.s0[r];
+                    if (a.il_s[r] == 0) a.il_s[r] = 1;  // empty range: never indexed
+                }
+            }
+            a.tm = q.tm;
+            a.key = philox_key(seed);
+            a.lc = log_consts();
+            a.first_sample = (uint32_t)(first_sample + q.s0);
+            a.n_tasks = q.n_tasks;
+            a.task_counter = &hd[g].task_counter;
+            a.edges = se[b];
+            a.weights = sw[b];
+            a.counts = q.counts;
+            a.spill_e = se[b] + slot_words;
+            a.spill_w = sw[b] ? sw[b] + wslots : nullptr;
+            a.spill_counter = &hd[g].spill_counter;
+            a.spill_cap = spill_cap;
+            a.spill_off = q.spill_off;
+            a.counters = hd[g].counters;
+            a.flags = &hd[g].flags;
+            a.check = env_i64("FM_DEBUG_CHECKS", 0) != 0;
+            a.counters_zeroed = 1;  // (hd is cleared at the start of every pass)
+            if (fuse) {
+                a.fuse = 1;
+                a.n_groups = n_batches;
+                a.grp_state = grp_state;
+                a.dest = q.dest;
+                a.discard = env_i64("FM_DISCARD", 1) != 0;
+                a.rank_map = a.rank_out ? p->cperm : nullptr;
+            }
         }
-        auto write_out = [&](int64_t cap, bool compact, bool rerun) -> cudaError_t {
-            cudaError_t e = compact ? launch_compact(cap, n_tasks, tm, counts, dest, spill_off, se, sw, a.spill_e,
-                                                     a.spill_w, (int2 *)own->edges, (int32_t *)own->weights,
-                                                     a.rank_out ? p->cperm : nullptr, a.ordered, ecm_rec ? 1 : 0, st)
-                                    : cudaSuccess;
-            if (e != cudaSuccess || !rerun) return e;
-            SampleArgs r = a;  // deterministic re-run of overflowed tasks straight into the final list
+        // compaction of group g into the list of capacity `cap` (+ the deterministic re-run of its
+        // overflowed tasks straight into the list, after the host knows the group bases)
+        // the TMA-staged small-footprint kernel is also the faster one alone (config 5: 4.07 vs 4.31 ms,
+        // config 2: 0.30 vs 0.34 ms) except with the rank -> id mapping of the rank-out path (its
+        // gathers sit in the store loop: config 4 2.5 vs 1.07 ms), where only the groups that run next
+        // to a sampler use it; FM_COMPACT_SMALL: 0 never, 2 always
+        auto use_small = [&](int64_t g) {
+            const int64_t mode = env_i64("FM_COMPACT_SMALL", 1);
+            return small_compact && (mode > 1 || g < G - 1 || !rank_out);
+        };
+        auto compact_group = [&](int64_t g, int64_t cap, cudaStream_t s) -> cudaError_t {
+            Group &q = grp[(size_t)g];
+            if (q.n_tasks == 0) return cudaSuccess;
+            return launch_compact(cap, q.n_tasks, q.tm, q.counts, q.dest, q.spill_off, q.a.edges, q.a.weights, q.a.spill_e,
+                                  q.a.spill_w, (int2 *)own->edges, (int32_t *)own->weights,
+                                  q.a.rank_out ? p->cperm : nullptr, q.a.ordered, ecm_rec ? 1 : 0,
+                                  use_small(g) ? 1 : 0, gbase + g, s);
+        };
+        auto rerun_group = [&](int64_t g, int64_t cap) -> cudaError_t {
+            Group &q = grp[(size_t)g];
+            SampleArgs r = q.a;
             r.fuse = 0;
-            r.n_tasks = n_tasks;
-            r.n_tasks_dev = &hd->n_overflow;
-            r.task_list = ovl;
-            r.rerun_base = dest;
+            r.counters_zeroed = 0;
+            r.n_tasks_dev = &hd[g].n_overflow;
+            r.task_list = q.ovl;
+            r.rerun_base = q.dest;
+            r.out_base = gbase_h[(size_t)g];
             r.out_cap = cap;
             r.edges = (int2 *)own->edges;
             r.weights = (int32_t *)own->weights;
             return launch_sample(model, r, st);
         };
         unsigned int plan_flags = 0;
-        // one pass of the call: sampler (+ copiers), offsets, overflow list; the host learns the total
-        // at the one synchronisation
+        // one pass of the call: every group queued, one synchronisation at the end
         auto run_pass = [&](int64_t cap) -> fm_status {
             CK(alloc_out(cap), "alloc edges");
-            PhaseTimer ts, tw;
-            if (fuse) {
-                CK(cudaMemsetAsync(grp_state, 0, sizeof(unsigned long long) * n_groups, st), "memset batch states");
-                CK(cudaMemsetAsync(hd, 0, sizeof(Hdr), st), "memset hdr");
-                a.out_e = (int2 *)own->edges;
-                a.out_w = (int32_t *)own->weights;
-                a.out_cap = cap;
+            CK(cudaMemsetAsync(hd, 0, sizeof(Hdr) * (size_t)G, st), "memset hdr");
+            CK(cudaMemsetAsync(gbase, 0, sizeof(int64_t) * ((size_t)G + 1), st), "memset group bases");
+            CK(cudaMemsetAsync(scan_tmp, 0, stb * (size_t)G, st), "memset scan words");
+            if (fuse) CK(cudaMemsetAsync(grp_state, 0, sizeof(unsigned long long) * n_batches, st), "memset batch states");
+            const bool timing = g_timing.load();
+            cudaEvent_t t_a = nullptr, t_b = nullptr, t_c = nullptr, ev_prev = nullptr;
+            if (timing) {
+                CK(new_event(&t_a, true), "event");
+                CK(new_event(&t_b, true), "event");
+                CK(new_event(&t_c, true), "event");
+                CK(cudaEventRecord(t_a, st), "event record");
             }
-            ts.begin(kPhaseSample, st);
-            CK(launch_sample(model, a, st), "sampler launch");
-            ts.end(st);
-            tw.begin(kPhaseWrite, st);
-            if (g_timing.load()) {
+            if (G > 1) {  // fork
+                cudaEvent_t ev;
+                CK(new_event(&ev, false), "event");
+                CK(cudaEventRecord(ev, st), "event record");
+                CK(cudaStreamWaitEvent(side, ev, 0), "fork");
+            }
+            // FM_PIPE_TRACE=1: a timeline of the groups' stages (stderr), from events on their streams
+            const bool ptrace = env_i64("FM_PIPE_TRACE", 0) != 0;
+            struct Mark {
+                int64_t g;
+                const char *what;
+                cudaEvent_t e;
+            };
+            std::vector<Mark> marks;
+            cudaEvent_t t_0 = nullptr;
+            auto mark = [&](int64_t g, const char *what, cudaStream_t s) {
+                if (!ptrace) return;
+                cudaEvent_t e;
+                if (new_event(&e, true) != cudaSuccess) return;
+                cudaEventRecord(e, s);
+                marks.push_back({g, what, e});
+            };
+            if (ptrace && new_event(&t_0, true) == cudaSuccess) cudaEventRecord(t_0, st);
+            for (int64_t g = 0; g < G; g++) {
+                Group &q = grp[(size_t)g];
+                cudaStream_t s = stream_of(g);
+                mark(g, "begin", s);
+                if (fuse) {
+                    q.a.out_e = (int2 *)own->edges;
+                    q.a.out_w = (int32_t *)own->weights;
+                    q.a.out_cap = cap;
+                }
+                if (q.n_tasks > 0) CK(launch_sample(model, q.a, s), "sampler launch");
+                mark(g, "sampled", s);
+                if (timing && g == G - 1) CK(cudaEventRecord(t_b, s), "event record");
+                if (q.n_tasks > 0 && !fuse)
+                    CK(scan_exclusive_i64(q.counts, q.dest, q.n_tasks, scan_tmp + stb * (size_t)g, stb, s, g < G - 1, true),
+                       "scan counts");
+                // the group's base is the running total of the preceding groups (the other stream)
+                if (ev_prev) CK(cudaStreamWaitEvent(s, ev_prev, 0), "wait for the preceding group's total");
+                if (q.n_tasks > 0) {
+                    CK(launch_offsets(q.R, q.tm, q.dest, offs_d + q.s0, gbase + g, gbase + g + 1, s), "offsets");
+                } else {
+                    CK(cudaMemcpyAsync(gbase + g + 1, gbase + g, sizeof(int64_t), cudaMemcpyDeviceToDevice, s), "base");
+                }
+                if (G > 1) {
+                    CK(new_event(&ev_prev, false), "event");
+                    CK(cudaEventRecord(ev_prev, s), "event record");
+                }
+                if (q.n_tasks > 0)
+                    CK(launch_overflow(q.n_tasks, q.tm, q.counts, q.spill_off, &hd[g].n_overflow, q.ovl, s),
+                       "overflow check");
+                // the final list was allocated up front (compaction and the re-run of overflowed tasks
+                // are queued without a host round trip)
+                mark(g, "scanned", s);
+                if (!fuse) CK(compact_group(g, cap, s), "compact");
+                mark(g, "compacted", s);
+            }
+            if (G > 1) {  // join
+                cudaEvent_t ev;
+                CK(new_event(&ev, false), "event");
+                CK(cudaEventRecord(ev, side), "event record");
+                CK(cudaStreamWaitEvent(st, ev, 0), "join");
+            }
+            if (timing) {
+                CK(cudaEventRecord(t_c, st), "event record");
+                // sampler phase = first sampler start .. last sampler end (the groups' samplers
+                // overlap each other and the preceding groups' compactions); write phase = the
+                // exposed remainder of the call
                 std::lock_guard<std::mutex> lk(g_tmu);
-                g_sample_launches++;
+                g_call_spans.push_back({t_a, t_b, t_c});  // (destroyed by fm_timing_get)
+                g_sample_launches += G;
+                for (auto &e : evs)
+                    if (e == t_a || e == t_b || e == t_c) e = nullptr;
             }
-            if (!fuse) CK(scan_exclusive_i64(counts, dest, n_tasks, scan_tmp, stb, st), "scan counts");
-            CK(launch_offsets(n_samples, tm, dest, offs_d, st), "offsets");
-            CK(launch_overflow(n_tasks, tm, counts, spill_off, &hd->n_overflow, ovl, st), "overflow check");
-            // the final list was allocated up front (compaction and the re-run of overflowed tasks are
-            // queued without a host round trip; one synchronisation at the end)
-            if (!fuse) CK(write_out(cap, true, false), "compact");
             CK(cudaMemcpyAsync(offsets_h, offs_d, sizeof(int64_t) * (n_samples + 1), cudaMemcpyDeviceToHost, st),
                "read offsets");
-            CK(cudaMemcpyAsync(&h, hd, sizeof(Hdr), cudaMemcpyDeviceToHost, st), "read hdr");
+            CK(cudaMemcpyAsync(h.data(), hd, sizeof(Hdr) * (size_t)G, cudaMemcpyDeviceToHost, st), "read hdr");
+            CK(cudaMemcpyAsync(gbase_h.data(), gbase, sizeof(int64_t) * ((size_t)G + 1), cudaMemcpyDeviceToHost, st),
+               "read group bases");
             // (pageable destinations: these reads are the call's synchronisation; the plan's flag word
             // is read here too, after every launch, not before the sampler)
             CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
                "read plan flags");
-            tw.end(st);
             CK(cudaStreamSynchronize(st), "sync (sample)");
+            if (ptrace && t_0) {
+                for (const Mark &m : marks) {
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, t_0, m.e);
+                    fprintf(stderr, "[pipe] group %lld %-9s %8.3f ms\n", (long long)m.g, m.what, ms);
+                }
+            }
             return FM_OK;
         };
         {
@@ -766,9 +986,15 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         fm::dump_trace();
 #endif
         fm::fuse_stats_dump();
+        unsigned int hflags = 0;
+        unsigned long long n_overflow = 0;
+        for (int64_t g = 0; g < G; g++) {
+            hflags |= h[(size_t)g].flags;
+            n_overflow += h[(size_t)g].n_overflow;
+        }
         if (plan_flags & kErrState) return fail(FM_ERR_STATE, "planner invariant violated (cuts)");
         // FM_DEBUG_CHECKS: a p > q contract violation fails the call; nothing stays allocated
-        if (h.flags & kErrBound) return fail(FM_ERR_BOUND, "p > q (1 + 2^-50) detected at a landed candidate (S:L289)");
+        if (hflags & kErrBound) return fail(FM_ERR_BOUND, "p > q (1 + 2^-50) detected at a landed candidate (S:L289)");
         const int64_t total = offsets_h[n_samples];
         {  // capacity hint for the next call on this plan
             const double per = (double)std::max<int64_t>(1, p->est_draws - p->n_seg) * (double)n_samples;
@@ -778,40 +1004,36 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             if (total > out_cap) pm->out_ratio = std::max(pm->out_ratio, seen * 1.02);
             else if (n_samples >= 8) pm->out_ratio = std::max(seen * 1.01, 0.05);
         }
-        if (total > out_cap) {  // the list was too small: redo the write into an exact-size list
+        if (total > out_cap) {
+            // the list was too small: the whole call again with an exact-size list (the scratch of
+            // the earlier groups is gone: double-buffered, or discarded by the fused copiers); rare:
+            // the plan's capacity hint covers every later call
             free_out();
             out_cap = total;
-            if (fuse) {  // the copiers consumed (discarded) the scratch: run the whole call again
-                fm_status r = run_pass(out_cap);
-                if (r != FM_OK) return r;
-                if (offsets_h[n_samples] != total) return fail(FM_ERR_STATE, "re-run total differs");
-                if (h.n_overflow > 0) {
-                    CK(write_out(out_cap, false, true), "rerun");
-                    CK(cudaStreamSynchronize(st), "sync (sample, rerun)");
-                }
-            } else {
-                CK(alloc_out(out_cap), "alloc edges");
-                CK(write_out(out_cap, true, h.n_overflow > 0), "compact / rerun");
-                CK(cudaStreamSynchronize(st), "sync (sample, exact)");
-            }
-        } else if (h.n_overflow > 0) {
-            CK(write_out(out_cap, false, true), "rerun");
+            fm_status r = run_pass(out_cap);
+            if (r != FM_OK) return r;
+            if (offsets_h[n_samples] != total) return fail(FM_ERR_STATE, "re-run total differs");
+        }
+        if (n_overflow > 0) {
+            for (int64_t g = 0; g < G; g++)
+                if (h[(size_t)g].n_overflow > 0) CK(rerun_group(g, out_cap), "rerun");
             CK(cudaStreamSynchronize(st), "sync (sample, rerun)");
         }
         out->n_edges = total;
+        out->flags = ((hflags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u) |
+                     (n_overflow ? FM_FLAG_SCRATCH_RERUN : 0u);
     }
     out->n_samples = n_samples;
     out->offsets = offsets_h;
     out->edges = (int32_t *)own->edges;
     out->weights = (int32_t *)own->weights;
     // every segment ends with exactly one terminal draw; every accepted edge is in the list
-    out->draws = (int64_t)h.counters[0];
+    out->draws = 0;
+    for (const Hdr &hg : h) out->draws += (int64_t)hg.counters[0];
     out->landed = out->draws - p->n_seg * n_samples;
     out->accepted = out->n_edges;
     out->segments = p->n_seg * n_samples;
     out->chunks = n_tasks;  // tasks of the call (coarse + fine lane-chunks)
-    out->flags = ((h.flags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u) |
-                 (h.n_overflow ? FM_FLAG_SCRATCH_RERUN : 0u);
     out->_owner = own;
     og.o = nullptr;
     {
@@ -882,7 +1104,9 @@ static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, 
                             uint64_t *rank_hist, fm_counters *out)
 {
     int64_t n_tasks = 0;
-    const TaskMap tm = make_task_map(p, n_samples, &n_tasks);
+    const int64_t kf = std::min(tail_samples(p, 0), n_samples);
+    const int64_t km = p->n_chunks[2] > 0 ? std::max<int64_t>(0, std::min(tail_samples(p, 2), n_samples) - kf) : 0;
+    const TaskMap tm = make_task_map(p, n_samples, kf, km, &n_tasks);
     if (n_tasks == 0) return FM_OK;
     Allocs tmp(st);
     struct Hdr {
@@ -1125,6 +1349,17 @@ fm_status fm_timing_get(fm_timing *t, int reset)
         cudaEventDestroy(pd.b);
     }
     g_pending.clear();
+    for (auto &sp : g_call_spans) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(sp.c) == cudaSuccess) {
+            if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) g_phase_ms[kPhaseSample] += ms;
+            if (cudaEventElapsedTime(&ms, sp.b, sp.c) == cudaSuccess) g_phase_ms[kPhaseWrite] += ms;
+        }
+        cudaEventDestroy(sp.a);
+        cudaEventDestroy(sp.b);
+        cudaEventDestroy(sp.c);
+    }
+    g_call_spans.clear();
     t->plan_ms = g_phase_ms[kPhasePlan];
     t->sample_ms = g_phase_ms[kPhaseSample];
     t->write_ms = g_phase_ms[kPhaseWrite];

@@ -62,11 +62,12 @@ struct Plan {
     unsigned char *rec; // [n_seg] packed records for the sampler, stride kRecStride(model) bytes
     int64_t est_draws;  // sum of segment work estimates / 2^G
     // chunking (does not change results)
-    // two chunkings: [0] coarse (most samples), [1] fine (the last samples of a call: short tail)
-    int64_t n_chunks[2];
-    int64_t *chunk_seg[2];   // [n_chunks+1] first segment of each lane-chunk
-    int64_t *chunk_cap[2];   // [n_chunks+1] exclusive prefix of the lane-chunk scratch slots (edges)
-    int64_t chunk_target[2]; // work per lane-chunk (units 2^G)
+    // three chunkings: [0] coarse, [1] fine (the last samples of a call: short tail), [2] big (the
+    // bulk of a call with many waves of work: fewer task switches; n_chunks[2] = 0: not built)
+    int64_t n_chunks[3];
+    int64_t *chunk_seg[3];   // [n_chunks+1] first segment of each lane-chunk
+    int64_t *chunk_cap[3];   // [n_chunks+1] exclusive prefix of the lane-chunk scratch slots (edges)
+    int64_t chunk_target[3]; // work per lane-chunk (units 2^G)
     int64_t wmax;         // bound of one segment's work (units 2^G)
     int64_t cap_per_sample;  // scratch edges per sample (upper bound of chunk_cap[n_chunks])
     bool slots_aligned;      // every scratch slot starts at a multiple of 4 edges (32 bytes)
@@ -152,7 +153,7 @@ void count_launch(int n = 1);
 // ------------------------------------------------------------------------------------------
 // exclusive prefix sum of int64 in[0..n) -> out[0..n], out[n] = total.  in == out allowed.
 cudaError_t scan_exclusive_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
-                               cudaStream_t st);
+                               cudaStream_t st, bool small = false, bool zeroed = false);
 size_t scan_tmp_bytes(int64_t n);
 // same for uint64
 cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes,

@@ -62,18 +62,24 @@ __global__ void k_pack_cand(int model, int64_t nc, const double *ckappa, const i
 // ------------------------------------------------------------------------------------------
 // sampler (fm_sample.cu)
 // ------------------------------------------------------------------------------------------
-// Task space of one fm_sample_* call: samples [0, s_split) use the coarse lane-chunks (index 0),
-// samples [s_split, R) the fine ones (index 1), so the end of the persistent queue consists of
-// short tasks (small end-of-launch tail).  Tasks are numbered sample-major in both ranges, hence
-// in canonical output order.
+// Task space of one fm_sample_* call (or sample group): three consecutive sample ranges, each with
+// its own lane-chunking of the plan -- range 0 the BIG chunks (most samples of a large call: fewer
+// task switches), range 1 the coarse ones, range 2 the fine ones (the last samples: the end of the
+// persistent queue consists of short tasks, small end-of-launch tail).  Tasks are numbered
+// sample-major within each range, hence in canonical output order.  Empty ranges are allowed.
+constexpr int kRanges = 3;
 struct TaskMap {
-    const int64_t *seg[2];  // chunk_seg of each chunking, [n_chunks + 1]
-    const int64_t *cap[2];  // exclusive prefix of the chunks' scratch slots, [n_chunks + 1]
-    int64_t n_chunks[2];
-    double inv_chunks[2];   // 1 / n_chunks (quotient estimate, corrected exactly below)
-    int64_t s_split, t_split;  // t_split = s_split * n_chunks[0]
+    const int64_t *seg[kRanges];  // chunk_seg of the range's chunking, [n_chunks + 1]
+    const int64_t *cap[kRanges];  // exclusive prefix of the chunks' scratch slots, [n_chunks + 1]
+    int64_t n_chunks[kRanges];
+    double inv_chunks[kRanges];   // 1 / n_chunks (quotient estimate, corrected exactly below)
+    int64_t s0[kRanges];          // first sample of each range (s0[0] = 0)
+    int64_t t0[kRanges];          // first task of each range (t0[0] = 0)
     int64_t cap_per_sample;
 };
+// (selects, not indexing by a run-time range: a dynamically indexed kernel parameter is copied to
+// local memory)
+#define FM_TM_SEL(M, field, k) ((k) == 0 ? (M).field[0] : (k) == 1 ? (M).field[1] : (M).field[2])
 
 // t = s n + c, 0 <= c < n, for t < 2^52: the fp64 quotient estimate is off by at most one
 __device__ __forceinline__ void divmod_est(int64_t t, int64_t n, double inv, int64_t &q, int64_t &r)
@@ -89,17 +95,21 @@ __device__ __forceinline__ void divmod_est(int64_t t, int64_t n, double inv, int
     }
 }
 
+__device__ __forceinline__ int task_range(const TaskMap &M, int64_t t) { return t >= M.t0[2] ? 2 : t >= M.t0[1] ? 1 : 0; }
+__device__ __forceinline__ int sample_range(const TaskMap &M, int64_t s) { return s >= M.s0[2] ? 2 : s >= M.s0[1] ? 1 : 0; }
+// first task of sample s (s = number of samples: the number of tasks)
+__device__ __forceinline__ int64_t sample_first_task(const TaskMap &M, int64_t s)
+{
+    const int k = sample_range(M, s);
+    return FM_TM_SEL(M, t0, k) + (s - FM_TM_SEL(M, s0, k)) * FM_TM_SEL(M, n_chunks, k);
+}
+
 __device__ __forceinline__ void task_decode(const TaskMap &M, int64_t t, int64_t &s, int64_t &c, int &k)
 {
-    if (t < M.t_split) {
-        k = 0;
-        divmod_est(t, M.n_chunks[0], M.inv_chunks[0], s, c);
-    } else {
-        k = 1;
-        int64_t s2;
-        divmod_est(t - M.t_split, M.n_chunks[1], M.inv_chunks[1], s2, c);
-        s = M.s_split + s2;
-    }
+    k = task_range(M, t);
+    int64_t s2;
+    divmod_est(t - FM_TM_SEL(M, t0, k), FM_TM_SEL(M, n_chunks, k), FM_TM_SEL(M, inv_chunks, k), s2, c);
+    s = FM_TM_SEL(M, s0, k) + s2;
 }
 
 // tasks per claim of the sampler's global queue (a warp batch; the fused write's unit)
@@ -119,16 +129,18 @@ struct SampleArgs {
     const int64_t *task_list;      // NULL: task = queue index; else task_list[queue index]
     int ordered;                   // bipartite / directed: emit (row id, candidate id) as is (R16)
     int rank_out;                  // UBCM: scratch pairs hold (row id, candidate rank), mapped by k_compact
-    int64_t il_s[2];               // > 0: queue order chunk-major within each chunking's samples (il_s[k]
+    int64_t il_s[kRanges];         // > 0: queue order chunk-major within each range's samples (il_s[k]
                                    // samples each), so the samples of one lane-chunk run together and
                                    // share its segment records in L2; 0: sample-major (queue = task)
     int buf4;                      // scratch slots 32-byte aligned: edges are written 4 at a time (whole sectors)
     unsigned long long *task_counter;  // global queue head (zeroed before each launch)
+    int counters_zeroed;           // the caller cleared task_counter and spill_counter (no memsets at the launch)
     int2 *edges;                   // scratch (normal) or final array (rerun)
     int32_t *weights;              // ECM
     const int64_t *rerun_base;     // rerun mode: per-task output base (final offsets); NULL otherwise
     const unsigned long long *n_tasks_dev;  // rerun mode: number of queued tasks, read on the device
     int64_t out_cap;               // rerun mode: capacity of the final list (writes beyond are dropped)
+    int64_t out_base;              // rerun mode: added to rerun_base[t] (the edges of the preceding sample groups)
     int64_t *counts;               // [n_samples * n_chunks] edges produced per task (normal mode)
     int2 *spill_e;                 // spill area for tasks that outgrow their slot (one region of
     int32_t *spill_w;              //   `cap` edges per task, bump-allocated)
@@ -163,8 +175,11 @@ cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *c
 cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w,
-                           const int32_t *rank_map, int ordered, int ecm_rec, cudaStream_t st);
-cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets, cudaStream_t st);
+                           const int32_t *rank_map, int ordered, int ecm_rec, int small, const int64_t *out_base,
+                           cudaStream_t st);
+// offsets[s] = *base_in + (first final position of sample s), s <= n_samples; *base_out = the running total
+cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets,
+                           const int64_t *base_in, int64_t *base_out, cudaStream_t st);
 // out[i] += in[i], i < n (uint64)
 cudaError_t launch_add_u64(const uint64_t *in, uint64_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_debug_eval(int fn, int64_t n, const double *in, double *out, cudaStream_t st);

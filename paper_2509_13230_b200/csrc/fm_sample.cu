@@ -67,6 +67,15 @@ namespace {
 constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
 constexpr int kBatch = kQueueBatch;  // tasks per warp batch
 
+// one sample range of the task map (TaskMap) for the sampler's shared-memory table
+struct RangeRec {
+    const int64_t *seg, *cap;
+    int64_t n_chunks;
+    double inv_chunks;
+    int64_t s0, t0, il_s;
+    double inv_il;  // 1 / il_s
+};
+
 // per-block copy of the log table: (invc, logc) pairs, one 16-byte lookup (8 conflict-free
 // copies, one per bank group, measured no faster: the lookups are not the bottleneck)
 struct LogSmem {
@@ -192,8 +201,8 @@ __device__ __forceinline__ void batch_copy(const SampleArgs &A, int64_t b, int64
             int64_t s_, c_;
             int k_;
             task_decode(A.tm, t, s_, c_, k_);
-            cap = A.tm.cap[k_][c_ + 1] - A.tm.cap[k_][c_];
-            src = s_ * A.tm.cap_per_sample + A.tm.cap[k_][c_];
+            cap = FM_TM_SEL(A.tm, cap, k_)[c_ + 1] - FM_TM_SEL(A.tm, cap, k_)[c_];
+            src = s_ * A.tm.cap_per_sample + FM_TM_SEL(A.tm, cap, k_)[c_];
             cnt = A.counts[t];
             sp = A.spill_off[t];
         }
@@ -315,11 +324,11 @@ __device__ __forceinline__ void batch_copy(const SampleArgs &A, int64_t b, int64
         for (int64_t s_ = s_first; s_ <= s_last; s_++) {
             // the batch's tasks of sample s_ are consecutive chunks of one chunking: their slots
             // form one contiguous range
-            const int kc = s_ == s_first ? k_first : s_ == s_last ? k_last : (s_ < A.tm.s_split ? 0 : 1);
+            const int kc = s_ == s_first ? k_first : s_ == s_last ? k_last : sample_range(A.tm, s_);
             const int64_t lo_c = s_ == s_first ? c_first : 0;
-            const int64_t hi_c = s_ == s_last ? c_last + 1 : A.tm.n_chunks[kc];
-            const size_t a = (size_t)(s_ * A.tm.cap_per_sample + A.tm.cap[kc][lo_c]) * sizeof(int2);
-            const size_t z = (size_t)(s_ * A.tm.cap_per_sample + A.tm.cap[kc][hi_c]) * sizeof(int2);
+            const int64_t hi_c = s_ == s_last ? c_last + 1 : FM_TM_SEL(A.tm, n_chunks, kc);
+            const size_t a = (size_t)(s_ * A.tm.cap_per_sample + FM_TM_SEL(A.tm, cap, kc)[lo_c]) * sizeof(int2);
+            const size_t z = (size_t)(s_ * A.tm.cap_per_sample + FM_TM_SEL(A.tm, cap, kc)[hi_c]) * sizeof(int2);
             const size_t la = (a + 127) & ~(size_t)127, lz = z & ~(size_t)127;
             for (size_t l = la + (size_t)lane * 128; l < lz; l += 32 * 128) discard_l2_line(base + l);
         }
@@ -384,8 +393,8 @@ __device__ __forceinline__ void batch_copy_tma(const SampleArgs &A, int64_t b, i
             int64_t s_, c_;
             int k_;
             task_decode(A.tm, t, s_, c_, k_);
-            cap = A.tm.cap[k_][c_ + 1] - A.tm.cap[k_][c_];
-            src = s_ * A.tm.cap_per_sample + A.tm.cap[k_][c_];
+            cap = FM_TM_SEL(A.tm, cap, k_)[c_ + 1] - FM_TM_SEL(A.tm, cap, k_)[c_];
+            src = s_ * A.tm.cap_per_sample + FM_TM_SEL(A.tm, cap, k_)[c_];
             cnt = A.counts[t];
             sp = A.spill_off[t];
         }
@@ -517,8 +526,8 @@ __device__ __forceinline__ unsigned sub_prep(const SampleArgs &A, int64_t tb, in
         int64_t s_, c_;
         int k_;
         task_decode(A.tm, t, s_, c_, k_);
-        cap = A.tm.cap[k_][c_ + 1] - A.tm.cap[k_][c_];
-        src = s_ * A.tm.cap_per_sample + A.tm.cap[k_][c_];
+        cap = FM_TM_SEL(A.tm, cap, k_)[c_ + 1] - FM_TM_SEL(A.tm, cap, k_)[c_];
+        src = s_ * A.tm.cap_per_sample + FM_TM_SEL(A.tm, cap, k_)[c_];
         cnt = A.counts[t];
         sp = A.spill_off[t];
     }
@@ -855,7 +864,22 @@ __global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : k
             }
         }
     }
-    const SmemLogTab T{A.lc, load_logtab()};
+    // the task map's three sample ranges as a table indexed by the range
+    __shared__ RangeRec s_rng[kRanges];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int r = 0; r < kRanges; r++) {
+            s_rng[r].seg = A.tm.seg[r];
+            s_rng[r].cap = A.tm.cap[r];
+            s_rng[r].n_chunks = A.tm.n_chunks[r];
+            s_rng[r].inv_chunks = A.tm.inv_chunks[r];
+            s_rng[r].s0 = A.tm.s0[r];
+            s_rng[r].t0 = A.tm.t0[r];
+            s_rng[r].il_s = A.il_s[r];
+            s_rng[r].inv_il = A.il_s[r] > 0 ? 1.0 / (double)A.il_s[r] : 0.0;
+        }
+    }
+    const SmemLogTab T{A.lc, load_logtab()};  // (block barrier inside)
     if constexpr (kFuse) {
         if ((threadIdx.x >> 5) == 0) {  // the block's copier warp
             // the staging buffer: dynamic shared memory after the sampler warps' prefetch slots
@@ -1123,25 +1147,30 @@ __global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : k
                 if (needc && !warp_done && my >= 0 && my < n_tasks) {
                     if (kFuse) s_tslot[threadIdx.x] = (unsigned char)myslot;
                     int64_t t = A.task_list ? A.task_list[my] : my;
+                    // the task's range record from the block's shared-memory table (one LDS per
+                    // field: selecting among the three ranges' parameters cost ~40 instructions)
                     if (A.il_s[0] > 0 && !A.task_list) {  // chunk-major queue -> canonical task index
-                        const int kq = my < A.tm.t_split ? 0 : 1;
-                        const int64_t m = kq ? my - A.tm.t_split : my, ns = A.il_s[kq];
-                        const int64_t cq = m / ns;
-                        t = (kq ? A.tm.t_split : 0) + (m - cq * ns) * A.tm.n_chunks[kq] + cq;
+                        const RangeRec &Q = s_rng[task_range(A.tm, my)];
+                        int64_t cq, sq;  // m = cq ns + sq (fp64 quotient estimate: no 64-bit division)
+                        divmod_est(my - Q.t0, Q.il_s, Q.inv_il, cq, sq);
+                        t = Q.t0 + sq * Q.n_chunks + cq;
                     }
+                    const RangeRec &Q = s_rng[task_range(A.tm, t)];
                     int64_t s, ch;
-                    int kk;
-                    task_decode(A.tm, t, s, ch, kk);
+                    divmod_est(t - Q.t0, Q.n_chunks, Q.inv_chunks, s, ch);
+                    s += Q.s0;
+                    const int64_t *seg_k = Q.seg, *cap_k = Q.cap;
                     s_task[ci] = t;
-                    g[c] = (int32_t)A.tm.seg[kk][ch];
-                    g_end[c] = (int32_t)A.tm.seg[kk][ch + 1];
+                    g[c] = (int32_t)seg_k[ch];
+                    g_end[c] = (int32_t)seg_k[ch + 1];
                     if (A.rerun_base) {
-                        const int64_t sl = A.rerun_base[t];
+                        const int64_t sl = A.rerun_base[t] + A.out_base;
                         eb[c] = A.edges + sl;
                         cap[c] = (int32_t)max((int64_t)0, min((int64_t)INT32_MAX, A.out_cap - sl));  // bounded by the list
                     } else {
-                        eb[c] = A.edges + (s * A.tm.cap_per_sample + A.tm.cap[kk][ch]);
-                        cap[c] = (int32_t)(A.tm.cap[kk][ch + 1] - A.tm.cap[kk][ch]);
+                        const int64_t c0 = cap_k[ch];
+                        eb[c] = A.edges + (s * A.tm.cap_per_sample + c0);
+                        cap[c] = (int32_t)(cap_k[ch + 1] - c0);
                     }
                     s_abs[c] = A.first_sample + (uint32_t)s;
                     cnt[c] = 0;
@@ -1420,16 +1449,17 @@ __device__ __forceinline__ bool task_overflowed(int64_t cnt, int64_t cap, int64_
     return cnt > cap && (cnt > 2 * cap || sp < 0);
 }
 
-__global__ void __launch_bounds__(256) k_overflow(int64_t n_tasks, const TaskMap tm, const int64_t *__restrict__ counts,
-                                                  const int64_t *__restrict__ spill_off, unsigned long long *n_overflow,
-                                                  int64_t *__restrict__ overflow_list)
+// (128 threads at <= 32 registers, like k_offsets: they fit next to the resident sampler blocks)
+__global__ void __launch_bounds__(128, 16) k_overflow(int64_t n_tasks, const TaskMap tm, const int64_t *__restrict__ counts,
+                                                      const int64_t *__restrict__ spill_off, unsigned long long *n_overflow,
+                                                      int64_t *__restrict__ overflow_list)
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tasks) return;
     int64_t s, c;
     int k;
     task_decode(tm, t, s, c, k);
-    if (task_overflowed(counts[t], tm.cap[k][c + 1] - tm.cap[k][c], spill_off[t])) {
+    if (task_overflowed(counts[t], FM_TM_SEL(tm, cap, k)[c + 1] - FM_TM_SEL(tm, cap, k)[c], spill_off[t])) {
         const unsigned long long o = atomicAdd(n_overflow, 1ull);
         overflow_list[o] = t;
     }
@@ -1452,7 +1482,7 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
                                                           const int2 *__restrict__ spe, const int32_t *__restrict__ spw,
                                                           int2 *__restrict__ oe, int32_t *__restrict__ ow,
                                                           int64_t out_cap, const int32_t *__restrict__ rank_map,
-                                                          int ordered)
+                                                          int ordered, const int64_t *__restrict__ out_base)
 {
     // rank_map: the scratch holds (row id, candidate rank): map the rank to its id and orient
     auto fin = [&](int2 v) -> int2 {
@@ -1471,14 +1501,14 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
             int64_t s, c;
             int k;
             task_decode(tm, t, s, c, k);
-            const int64_t cap = tm.cap[k][c + 1] - tm.cap[k][c];
+            const int64_t cap = FM_TM_SEL(tm, cap, k)[c + 1] - FM_TM_SEL(tm, cap, k)[c];
             const int64_t cnt = counts[t];
             sp = spill_off[t];
-            dst = dest[t];
+            dst = dest[t] + (out_base ? *out_base : 0);  // (+ the edges of the preceding sample groups)
             // tasks that would land beyond the list are dropped: the host sees the total and redoes the write
             cn = task_overflowed(cnt, cap, sp) || dst + cnt > out_cap ? 0 : (int32_t)cnt;
             cp = (int32_t)cap;
-            src = s * tm.cap_per_sample + tm.cap[k][c];
+            src = s * tm.cap_per_sample + FM_TM_SEL(tm, cap, k)[c];
         }
         s_src[threadIdx.x] = src;
         s_dst[threadIdx.x] = dst;
@@ -1555,13 +1585,243 @@ __global__ void __launch_bounds__(kCopyThreads) k_compact(int64_t n_tasks, const
     }
 }
 
-__global__ void k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__restrict__ dest,
-                          int64_t *__restrict__ offsets)
+// Compaction with a small footprint (128 threads, <= 32 registers, 48 KB of shared memory): one
+// such block fits into the 4096 registers per SM that three 256-thread sampler blocks at 80
+// registers leave free (the sampler's shared-memory carveout leaves it room), so the compaction
+// of sample group g runs NEXT TO the persistent sampler of group g + 1 on every SM (DESIGN.md
+// 12.3: HBM is ~10 % busy under the sampler).  With so few registers -- and with the SM's
+// load/store path busy with the sampler's gathers -- the bytes in flight go through the TMA
+// engine: each warp copies 32 consecutive tasks (lane l holds task l's slot, final position and
+// count); per round the next tasks whose slots fit one 6 KB staging buffer are loaded by ONE
+// cp.async.bulk per task (issued by the task's own lane, completing on the buffer's mbarrier),
+// double-buffered, and the warp stores a landed round task by task with aligned 16-byte stores
+// (a task at an odd final position: its first edge alone, then pairs re-aligned through shared
+// memory).  Slots must be 32-byte aligned (Plan::slots_aligned).  *out_base (device) is added to
+// every final position: the edges of the preceding sample groups.
+constexpr int kC2Threads = 128, kC2Buf = 6144;
+constexpr int kC2Smem = (kC2Threads / 32) * (2 * kC2Buf + 16);  // bytes per block (dynamic)
+#ifdef FM_C2_STATS  // instrumentation build: blocks and block time per SM, first start / last end
+__device__ unsigned long long g_c2[256][2];
+__device__ unsigned long long g_c2t[2] = {~0ull, 0ull};
+#endif
+template <bool kMap, bool kRec>
+__global__ void __launch_bounds__(kC2Threads, 16) k_compact2(int64_t n_tasks, const TaskMap tm,
+                                                             const int64_t *__restrict__ counts,
+                                                             const int64_t *__restrict__ dest,
+                                                             const int64_t *__restrict__ spill_off,
+                                                             const int4 *__restrict__ se4, const int2 *__restrict__ spe,
+                                                             const int32_t *__restrict__ spw, int2 *__restrict__ oe,
+                                                             int32_t *__restrict__ ow, int64_t out_cap,
+                                                             const int32_t *__restrict__ rank_map, int ordered,
+                                                             const int64_t *__restrict__ out_base)
+{
+    extern __shared__ __align__(128) unsigned char s_c2[];
+#ifdef FM_C2_STATS
+    unsigned long long c2_t0 = 0;
+    {
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(c2_t0));
+        if (threadIdx.x == 0) atomicMin(&g_c2t[0], c2_t0);
+    }
+#endif
+    const int lane = threadIdx.x & 31;
+    const int64_t t0 = ((int64_t)blockIdx.x * (kC2Threads / 32) + (threadIdx.x >> 5)) * 32;
+    if (t0 >= n_tasks) return;  // (warp-uniform; the kernel has no block barrier)
+    // this warp's two staging buffers and their mbarriers
+    const uint32_t buf0 = (uint32_t)__cvta_generic_to_shared(s_c2) + (threadIdx.x >> 5) * (2 * kC2Buf + 16);
+    const uint32_t mb0 = buf0 + 2 * kC2Buf;
+    if (lane == 0) {
+        mbar_init(mb0, 1);
+        mbar_init(mb0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const int64_t t = t0 + lane;
+    const int64_t base = out_base ? *out_base : 0;
+    int64_t src = 0, dst = base;
+    int32_t n1 = 0;
+    bool spilled = false;
+    if (t < n_tasks) {
+        int64_t s, c;
+        int kr;
+        task_decode(tm, t, s, c, kr);
+        const int64_t *capp = FM_TM_SEL(tm, cap, kr);
+        const int64_t c0 = capp[c];
+        const int64_t cap = capp[c + 1] - c0;
+        const int64_t cnt = counts[t];
+        dst = dest[t] + base;
+        // tasks that would land beyond the list are dropped: the host sees the total and redoes the write
+        const bool drop = task_overflowed(cnt, cap, spill_off[t]) || dst + cnt > out_cap;
+        n1 = drop ? 0 : (int32_t)min(cnt, cap);
+        spilled = !drop && cnt > cap;
+        src = s * tm.cap_per_sample + c0;
+    }
+    // staged bytes of the task's slot part: whole 16-byte units (a slot is a multiple of 32 bytes)
+    const uint32_t bytes = kRec ? (uint32_t)n1 * 16u : (uint32_t)((n1 + 1) & ~1) * 8u;
+    const char *gsrc = reinterpret_cast<const char *>(se4) + (size_t)src * (kRec ? 16 : 8);
+    __syncwarp();
+    // store the staged task (final position d, n elements, staged at shared address sa), warp-wide
+    auto store_task = [&](int64_t d, int32_t n, uint32_t sa) {
+        if (kRec) {
+            for (int32_t e = lane; e < n; e += 32) {
+                int4 v;
+                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(sa + e * 16));
+                __stcs(oe + d + e, make_int2(v.x, v.y));
+                __stcs(ow + d + e, v.z);
+            }
+            return;
+        }
+        // pairs (e, e + 1) at even final positions: e = odd + 2 lane, ... (odd: element 0 alone first)
+        const int32_t odd = (int32_t)(d & 1);
+        if (odd && lane == 0) {
+            int2 v;
+            asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(sa));
+            if (kMap) {
+                v.y = __ldg(rank_map + v.y);
+                if (!ordered) v = make_int2(min(v.x, v.y), max(v.x, v.y));
+            }
+            __stcs(oe + d, v);
+        }
+        for (int32_t e = odd + 2 * lane; e < n; e += 64) {
+            int4 v;
+            if (odd) {
+                asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(sa + e * 8));
+                if (e + 1 < n) asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v.z), "=r"(v.w) : "r"(sa + e * 8 + 8));
+            } else {
+                asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(sa + e * 8));
+            }
+            if (kMap) {  // (row id, candidate rank) -> the candidate's id, oriented
+                v.y = __ldg(rank_map + v.y);
+                if (e + 1 < n) v.w = __ldg(rank_map + v.w);
+                if (!ordered) v = make_int4(min(v.x, v.y), max(v.x, v.y), min(v.z, v.w), max(v.z, v.w));
+            }
+            if (e + 1 < n) __stcs(reinterpret_cast<int4 *>(oe + d + e), v);
+            else __stcs(oe + d + e, make_int2(v.x, v.y));
+        }
+    };
+    // (rare) a slot part larger than a staging buffer: plain warp copy
+    {
+        unsigned big = __ballot_sync(0xffffffffu, n1 > 0 && bytes > (uint32_t)kC2Buf);
+        while (big) {
+            const int k = __ffs(big) - 1;
+            big &= big - 1;
+            const int64_t d_k = __shfl_sync(0xffffffffu, dst, k), s_k = __shfl_sync(0xffffffffu, src, k);
+            const int32_t n_k = __shfl_sync(0xffffffffu, n1, k);
+            for (int32_t e = lane; e < n_k; e += 32) {
+                if (kRec) {
+                    const int4 v = se4[s_k + e];
+                    oe[d_k + e] = make_int2(v.x, v.y);
+                    ow[d_k + e] = v.z;
+                } else {
+                    int2 v = reinterpret_cast<const int2 *>(se4)[s_k + e];
+                    if (kMap) {
+                        v.y = __ldg(rank_map + v.y);
+                        if (!ordered) v = make_int2(min(v.x, v.y), max(v.x, v.y));
+                    }
+                    oe[d_k + e] = v;
+                }
+            }
+        }
+    }
+    bool pending = n1 > 0 && bytes <= (uint32_t)kC2Buf;
+    // two-stage pipeline over rounds: round r's loads are issued into buffer r & 1, then round r - 1
+    // (the other buffer) is awaited and stored
+    bool p_mine = false;     // this lane's task is in the round in flight
+    uint32_t p_off = 0;      //   at this offset of its buffer
+    int p_buf = 0, r = 0;
+    bool p_any = false;
+    unsigned ph = 0;         // bit b: phase parity of buffer b's mbarrier
+    for (;;) {
+        const bool any = __any_sync(0xffffffffu, pending);
+        if (!any && !p_any) break;
+        bool mine = false;
+        uint32_t off = 0;
+        const int b = r & 1;
+        if (any) {
+            // this round: the pending tasks, in lane order, whose staging ranges fit the buffer
+            const uint32_t sz = pending ? bytes : 0u;
+            uint32_t inc = sz;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            off = inc - sz;
+            mine = pending && inc <= (uint32_t)kC2Buf;  // (the first pending task always fits)
+            const uint32_t total = __reduce_add_sync(0xffffffffu, mine ? sz : 0u);
+            // buffer b was last read by the stores of round r - 2 (generic proxy): order the
+            // async-proxy writes after them
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect(mb0 + 8 * b, total);
+            __syncwarp();
+            if (mine) bulk_g2s(buf0 + b * kC2Buf + off, gsrc, bytes, mb0 + 8 * b);
+            pending = pending && !mine;
+        }
+        if (p_any) {  // finish the previous round
+            mbar_wait(mb0 + 8 * p_buf, (ph >> p_buf) & 1u);
+            ph ^= 1u << p_buf;
+            unsigned m = __ballot_sync(0xffffffffu, p_mine);
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                store_task(__shfl_sync(0xffffffffu, dst, k), __shfl_sync(0xffffffffu, n1, k),
+                           buf0 + p_buf * kC2Buf + __shfl_sync(0xffffffffu, p_off, k));
+            }
+            __syncwarp();
+        }
+        p_any = any;
+        p_mine = mine;
+        p_off = off;
+        p_buf = b;
+        r++;
+    }
+#ifdef FM_C2_STATS
+    if (threadIdx.x == 0) {
+        unsigned long long t1;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+        atomicAdd(&g_c2[sm][0], 1ull);
+        atomicAdd(&g_c2[sm][1], t1 - c2_t0);
+        atomicMax(&g_c2t[1], t1);
+    }
+#endif
+    // spilled tails (rare): the task's lane re-reads its metadata, the warp copies
+    unsigned m = __ballot_sync(0xffffffffu, spilled);
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t tk = t0 + k;
+        int64_t s, c;
+        int kr;
+        task_decode(tm, tk, s, c, kr);
+        const int64_t *capp = FM_TM_SEL(tm, cap, kr);
+        const int64_t cap = capp[c + 1] - capp[c];
+        const int64_t cnt = counts[tk], sp = spill_off[tk];
+        const int64_t d_k = dest[tk] + base;
+        for (int64_t i = cap + lane; i < cnt; i += 32) {
+            int2 ev = spe[sp + i - cap];
+            if (kMap) {
+                const int32_t id = __ldg(rank_map + ev.y);
+                ev = ordered ? make_int2(ev.x, id) : make_int2(min(ev.x, id), max(ev.x, id));
+            }
+            oe[d_k + i] = ev;
+            if (kRec) ow[d_k + i] = spw[sp + i - cap];
+        }
+    }
+}
+
+// per-sample offsets of a sample group: offsets[s] = base + dest[first task of sample s], and the
+// running total for the next group, base_next = base + dest[n_tasks]
+__global__ void __launch_bounds__(128, 16) k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__restrict__ dest,
+                                                     int64_t *__restrict__ offsets, const int64_t *__restrict__ base_in,
+                                                     int64_t *base_out)
 {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s > n_samples) return;
-    const int64_t t0 = s <= tm.s_split ? s * tm.n_chunks[0] : tm.t_split + (s - tm.s_split) * tm.n_chunks[1];
-    offsets[s] = dest[t0];  // dest[n_tasks] is the total
+    const int64_t base = base_in ? *base_in : 0;
+    const int64_t v = base + dest[sample_first_task(tm, s)];  // dest[n_tasks] is the group's total
+    offsets[s] = v;
+    if (s == n_samples && base_out) *base_out = v;
 }
 
 __global__ void k_add_u64(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, int64_t n)
@@ -1629,6 +1889,29 @@ void dump_trace()
 
 void fuse_stats_dump()
 {
+#ifdef FM_C2_STATS
+    {
+        static unsigned long long h[256][2], ht[2];
+        if (cudaMemcpyFromSymbol(h, g_c2, sizeof(h)) == cudaSuccess && cudaMemcpyFromSymbol(ht, g_c2t, sizeof(ht)) == cudaSuccess) {
+            unsigned long long nb = 0, tt = 0, mn = ~0ull, mx = 0;
+            int used = 0;
+            for (int i = 0; i < 256; i++) {
+                nb += h[i][0];
+                tt += h[i][1];
+                if (h[i][0]) {
+                    used++;
+                    mn = h[i][0] < mn ? h[i][0] : mn;
+                    mx = h[i][0] > mx ? h[i][0] : mx;
+                }
+            }
+            fprintf(stderr, "[c2] blocks %llu on %d SMs (min %llu max %llu per SM), mean block time %.1f us, span %.3f ms\n", nb, used,
+                    mn, mx, nb ? 1e-3 * (double)tt / (double)nb : 0.0, 1e-6 * (double)(ht[1] - ht[0]));
+            static unsigned long long z[256][2], zt[2] = {~0ull, 0ull};
+            cudaMemcpyToSymbol(g_c2, z, sizeof(z));
+            cudaMemcpyToSymbol(g_c2t, zt, sizeof(zt));
+        }
+    }
+#endif
 #ifdef FM_FUSE_STATS
     unsigned long long h[8];
     if (cudaMemcpyFromSymbol(h, g_fstats, sizeof(h)) != cudaSuccess) return;
@@ -1684,7 +1967,8 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         int carve = cv && *cv ? atoi(cv) : 40;
         cudaFuncAttributes fa;
         if (carve >= 0 && cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
-            const size_t need = (size_t)(kFuse ? 1 : kMinB) * (fa.sharedSizeBytes + dyn + 1024);
+            // (+ one co-resident small-footprint compaction block of the pipelined sample groups)
+            const size_t need = (size_t)(kFuse ? 1 : kMinB) * (fa.sharedSizeBytes + dyn + 1024) + kC2Smem + 2048;
             const int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
             carve = std::max(carve, std::min(pct, 100));
         }
@@ -1731,9 +2015,11 @@ cudaError_t launch_sample(int model, const SampleArgs &a, cudaStream_t st)
     if (a.n_tasks <= 0) return cudaSuccess;
     cudaError_t e = ensure_log_table(st);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(a.task_counter, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
-    if (a.spill_counter && !a.rerun_base) {
+    if (!a.counters_zeroed) {
+        e = cudaMemsetAsync(a.task_counter, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+    }
+    if (a.spill_counter && !a.rerun_base && !a.counters_zeroed) {
         e = cudaMemsetAsync(a.spill_counter, 0, sizeof(unsigned long long), st);
         if (e != cudaSuccess) return e;
     }
@@ -1756,7 +2042,7 @@ cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *c
 {
     if (n_tasks <= 0) return cudaSuccess;
     count_launch();
-    k_overflow<<<(unsigned)((n_tasks + 255) / 256), 256, 0, st>>>(n_tasks, tm, counts, spill_off, n_overflow,
+    k_overflow<<<(unsigned)((n_tasks + 127) / 128), 128, 0, st>>>(n_tasks, tm, counts, spill_off, n_overflow,
                                                                  overflow_list);
     return cudaGetLastError();
 }
@@ -1764,30 +2050,47 @@ cudaError_t launch_overflow(int64_t n_tasks, const TaskMap &tm, const int64_t *c
 cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, const int64_t *counts, const int64_t *dest,
                            const int64_t *spill_off, const int2 *scratch_e, const int32_t *scratch_w,
                            const int2 *spill_e, const int32_t *spill_w, int2 *out_e, int32_t *out_w,
-                           const int32_t *rank_map, int ordered, int ecm_rec, cudaStream_t st)
+                           const int32_t *rank_map, int ordered, int ecm_rec, int small, const int64_t *out_base,
+                           cudaStream_t st)
 {
     if (n_tasks <= 0 || out_cap <= 0) return cudaSuccess;
     count_launch();
+    if (small) {
+        // small-footprint kernel (aligned slots; UBCM pairs or ECM records): co-resident with the sampler
+        const unsigned grid = (unsigned)((n_tasks + kC2Threads - 1) / kC2Threads);
+        const int4 *se4 = reinterpret_cast<const int4 *>(scratch_e);
+        auto go = [&](auto kern) -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kC2Smem);
+            if (e != cudaSuccess) return e;
+            kern<<<grid, kC2Threads, kC2Smem, st>>>(n_tasks, tm, counts, dest, spill_off, se4, spill_e, spill_w, out_e, out_w,
+                                                    out_cap, rank_map, ordered, out_base);
+            return cudaGetLastError();
+        };
+        if (rank_map) return go(k_compact2<true, false>);
+        if (ecm_rec) return go(k_compact2<false, true>);
+        return go(k_compact2<false, false>);
+    }
     const unsigned grid = (unsigned)((n_tasks + kCopyThreads - 1) / kCopyThreads);
     if (rank_map)
         k_compact<true, false><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e,
                                                               scratch_w, spill_e, spill_w, out_e, out_w, out_cap,
-                                                              rank_map, ordered);
+                                                              rank_map, ordered, out_base);
     else if (ecm_rec)
         k_compact<false, true><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e,
                                                               scratch_w, spill_e, spill_w, out_e, out_w, out_cap,
-                                                              rank_map, ordered);
+                                                              rank_map, ordered, out_base);
     else
         k_compact<false, false><<<grid, kCopyThreads, 0, st>>>(n_tasks, tm, counts, dest, spill_off, scratch_e,
                                                                scratch_w, spill_e, spill_w, out_e, out_w, out_cap,
-                                                               rank_map, ordered);
+                                                               rank_map, ordered, out_base);
     return cudaGetLastError();
 }
 
-cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets, cudaStream_t st)
+cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets,
+                           const int64_t *base_in, int64_t *base_out, cudaStream_t st)
 {
     count_launch();
-    k_offsets<<<(unsigned)((n_samples + 1 + 255) / 256), 256, 0, st>>>(n_samples, tm, dest, offsets);
+    k_offsets<<<(unsigned)((n_samples + 1 + 127) / 128), 128, 0, st>>>(n_samples, tm, dest, offsets, base_in, base_out);
     return cudaGetLastError();
 }
 

@@ -30,11 +30,11 @@ struct MaxF64 {
 template <bool kRev>
 __device__ __forceinline__ int64_t phys(int64_t i, int64_t n) { return kRev ? n - 1 - i : i; }
 
-template <typename Op>
+template <typename Op, int kT = kThreads>
 __device__ __forceinline__ typename Op::T block_exclusive(typename Op::T v, typename Op::T *total)
 {
     using T = typename Op::T;
-    __shared__ T warp_tot[kThreads / 32];
+    __shared__ T warp_tot[kT / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T inc = v;
 #pragma unroll
@@ -46,7 +46,7 @@ __device__ __forceinline__ typename Op::T block_exclusive(typename Op::T v, type
     __syncthreads();
     T wpre = Op::id(), all = Op::id();
 #pragma unroll
-    for (int w = 0; w < kThreads / 32; w++) {
+    for (int w = 0; w < kT / 32; w++) {
         if (w < wid) wpre = Op::op(wpre, warp_tot[w]);
         all = Op::op(all, warp_tot[w]);
     }
@@ -154,9 +154,13 @@ __global__ void k_set_f64(double *p, double v) { *p = v; }
 // sums here are non-negative and < 2^62).  status[] and the ticket counter start at zero.
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64_t *out, int64_t n,
-                                                      uint64_t *status, unsigned int *ticket)
+// kT = 128 with <= 32 registers (kMinB = 16) is the small-footprint variant: one such block fits
+// next to three resident sampler blocks per SM (the pipelined sample groups).
+template <int kT, int kMinB>
+__global__ void __launch_bounds__(kT, kMinB) k_scan_lb(const uint64_t *in, uint64_t *out, int64_t n,
+                                                       uint64_t *status, unsigned int *ticket)
 {
+    constexpr int kTile = kT * kItems;
     __shared__ unsigned int s_tile;
     __shared__ uint64_t s_prefix;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64
 #pragma unroll
     for (int k = 0; k < kItems; k++) acc += v[k];
     uint64_t tot;
-    const uint64_t exc = block_exclusive<SumU64>(acc, &tot);
+    const uint64_t exc = block_exclusive<SumU64, kT>(acc, &tot);
     if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
         const int lane = threadIdx.x;
         uint64_t prefix = 0;
@@ -236,28 +240,37 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(const uint64_t *in, uint64
     if (tile == (n - 1) / kTile && threadIdx.x == ((n - 1) % kTile) / kItems) out[n] = pre;  // total
 }
 
-cudaError_t run_scan_lb(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes, cudaStream_t st)
+cudaError_t run_scan_lb(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes, cudaStream_t st,
+                        bool small = false, bool zeroed = false)
 {
-    const int64_t nb = (n + kTile - 1) / kTile;
+    const int64_t tile = small ? 128 * kItems : kTile;
+    const int64_t nb = (n + tile - 1) / tile;
     const size_t need = sizeof(uint64_t) * (size_t)(nb + 1);
     if (tmp_bytes < need) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemsetAsync(tmp, 0, need, st);
+    // (zeroed: the caller cleared tmp -- the pipelined sample groups clear every group's words up
+    // front: a memset between the groups' kernels would wait for the resident sampler)
+    cudaError_t e = zeroed ? cudaSuccess : cudaMemsetAsync(tmp, 0, need, st);
     if (e != cudaSuccess) return e;
     count_launch();
-    k_scan_lb<<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, (uint64_t *)tmp, (unsigned int *)((uint64_t *)tmp + nb));
+    if (small)
+        k_scan_lb<128, 16><<<(unsigned)nb, 128, 0, st>>>(in, out, n, (uint64_t *)tmp, (unsigned int *)((uint64_t *)tmp + nb));
+    else
+        k_scan_lb<kThreads, 1><<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, (uint64_t *)tmp,
+                                                                  (unsigned int *)((uint64_t *)tmp + nb));
     return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t scan_tmp_bytes(int64_t n) { return sizeof(int64_t) * (size_t)((n + kTile - 1) / kTile + 2); }
+// (sized for the small-footprint variant's 1024-item tiles)
+size_t scan_tmp_bytes(int64_t n) { return sizeof(int64_t) * (size_t)((n + 1023) / 1024 + 2); }
 
 // non-negative sums only (all callers): one launch + one memset
 cudaError_t scan_exclusive_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, size_t tmp_bytes,
-                               cudaStream_t st)
+                               cudaStream_t st, bool small, bool zeroed)
 {
     if (n == 0) return cudaMemsetAsync(out, 0, sizeof(int64_t), st);
-    return run_scan_lb((const uint64_t *)in, (uint64_t *)out, n, tmp, tmp_bytes, st);
+    return run_scan_lb((const uint64_t *)in, (uint64_t *)out, n, tmp, tmp_bytes, st, small, zeroed);
 }
 
 cudaError_t scan_exclusive_u64(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes,

@@ -1,0 +1,14 @@
+# full GPU suite + default bench lines of every config
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+if [ -z "$SKIP_TESTS" ]; then python -m pytest tests -m gpu -q -x -p no:cacheprovider --timeout 1500 > gpurun_out/pytest.log 2>&1; fi
+echo "pytest rc=$?"; tail -3 gpurun_out/pytest.log
+python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
+for cfg in 5 4 2 3; do
+  timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg${cfg}.json 2>gpurun_out/bench_cfg${cfg}.err
+  python - <<PY
+import json
+d=json.loads(open("gpurun_out/bench_cfg${cfg}.json").read().strip().splitlines()[-1])
+print("cfg ${cfg}", round(d["value"]/1e9,2), "Gedges/s", round(d["ms_per_step"],3), "ms", {k: round(v,3) for k,v in d["phase_ms_per_step"].items()}, "frac", round(d["roofline"]["frac"],3), "call", round(d["roofline"]["call"]["frac"],3))
+PY
+done

@@ -237,3 +237,57 @@ def test_fused_write_option_parity(O, n, S, R):
     assert np.array_equal(e.offsets, e0.offsets) and np.array_equal(E, E0)
     ref = O.sample(O.sort_plan(x, seg_target=S), 4242, n_samples=R, first_sample=1, nthreads=O.ncores())
     assert np.array_equal(E, ref.edges)
+
+
+# ------------------------------------------------------------------------------ round-2 scheduling options
+@pytest.mark.parametrize("ecm", [False, True])
+@pytest.mark.parametrize("env", [
+    {"FM_SAMPLE_GROUPS": "3"},                              # pipelined sample groups on two streams
+    {"FM_SAMPLE_GROUPS": "4", "FM_COMPACT_SMALL": "2"},     # ... every group through the TMA compaction
+    {"FM_COMPACT_SMALL": "0"},                              # the block-staged compaction kernel
+    {"FM_CHUNK_BIG_DRAWS": "0"},                            # no big lane-chunks
+    {"FM_CHUNK_BIG_DRAWS": "512", "FM_TAIL_FACTOR_BIG": "0", "FM_TAIL_FACTOR": "0"},  # big chunks only
+    {"FM_CHUNK_BIG_DRAWS": "300", "FM_TAIL_FACTOR_BIG": "0", "FM_SAMPLE_GROUPS": "2",
+     "FM_UBCM_RANK_OUT_MIN": "0"},                          # all three ranges x groups x rank mapping
+])
+def test_scheduling_options_identical(O, monkeypatch, ecm, env):
+    """Sample groups, the lane-chunkings (big / coarse / fine) and the compaction kernels only
+    schedule work: offsets, edges and weights equal the default configuration's byte for byte, and
+    the oracle's canonical order."""
+    x, y = WL.random_fitness(17, 30_011, 2.4, 0.02, ecm=True)
+    yy = y if ecm else None
+    R = 9
+    _, e0, E0, W0 = gpu_run(x, yy, 64, 31, R, first_sample=2)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    try:
+        plan, e, E, W = gpu_run(x, yy, 64, 31, R, first_sample=2)
+    finally:
+        for k in env:
+            monkeypatch.delenv(k)
+    assert np.array_equal(e.offsets, e0.offsets) and np.array_equal(E, E0)
+    assert (e.draws, e.landed, e.accepted) == (e0.draws, e0.landed, e0.accepted)
+    if ecm:
+        assert np.array_equal(W, W0)
+    ref = O.sample(O.sort_plan(x, yy, seg_target=64), 31, n_samples=R, first_sample=2, nthreads=O.ncores())
+    assert np.array_equal(e.offsets, ref.offsets) and np.array_equal(E, ref.edges)
+    if ecm:
+        assert np.array_equal(W, ref.weights)
+
+
+def test_groups_with_overflow_rerun(monkeypatch):
+    """Sample groups + tasks that overflow slot and spill (re-run into the final list at the group's
+    base) + a final list that is too small on the first pass (whole call redone)."""
+    x, _ = WL.random_fitness(6, 20_000, 2.3, 0.02)
+    _, e, E, _ = gpu_run(x, None, 64, 5, 6)
+    monkeypatch.setenv("FM_DEBUG_SCRATCH_CAP", "8")
+    monkeypatch.setenv("FM_SAMPLE_GROUPS", "3")
+    _, e2, E2, _ = gpu_run(x, None, 64, 5, 6)
+    monkeypatch.delenv("FM_DEBUG_SCRATCH_CAP")
+    monkeypatch.delenv("FM_SAMPLE_GROUPS")
+    assert e2.flags & fm.FM_FLAG_SCRATCH_RERUN
+    assert np.array_equal(e.offsets, e2.offsets)
+    key = lambda A: np.sort(A.view(np.int64).ravel())  # noqa: E731
+    for s in range(6):
+        a, b = e.offsets[s], e.offsets[s + 1]
+        assert np.array_equal(key(E[a:b]), key(E2[a:b]))
