@@ -13,6 +13,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: host ranges around every entry point (no-ops without a tool)
+
 #include "fm_internal.cuh"
 #include "fm_plan_kernels.cuh"
 
@@ -70,6 +72,12 @@ struct PhaseTimer {
         g_pending.push_back({phase, a, b});
         phase = -1;
     }
+};
+
+// NVTX range of an entry point (or a phase inside it): visible in Nsight Systems / Compute timelines
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 thread_local std::string g_err;
@@ -299,6 +307,7 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
                                 int64_t n2, const double *x2, const double *y2, int64_t seg_target,
                                 void *cuda_stream, fm_plan **plan_out)
 {
+    NvtxRange nvtx_("fm_sort_plan (a1-a4)");
     if (!plan_out) return fail(FM_ERR_INVALID, "plan_out is NULL");
     *plan_out = nullptr;
     if (model != FM_UBCM && model != FM_ECM) return fail(FM_ERR_INVALID, "unknown model %d", (int)model);
@@ -600,6 +609,7 @@ static int64_t tail_samples(const Plan *p, int k)
 static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
                              uint32_t flags, void *cuda_stream, fm_edges *out)
 {
+    NvtxRange nvtx_(model == FM_UBCM ? "fm_sample_ubcm (a5-a6)" : "fm_sample_ecm (a5-a6)");
     if (!out) return fail(FM_ERR_INVALID, "out is NULL");
     memset(out, 0, sizeof(*out));
     if (!plan_ || !plan_live(plan_)) return fail(FM_ERR_STATE, "not a live fm_plan");
@@ -968,7 +978,10 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             // is read here too, after every launch, not before the sampler)
             CK(cudaMemcpyAsync(&plan_flags, p->dev_flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st),
                "read plan flags");
-            CK(cudaStreamSynchronize(st), "sync (sample)");
+            {
+                NvtxRange nvtx_w("fm_sample: wait for the device");
+                CK(cudaStreamSynchronize(st), "sync (sample)");
+            }
             if (ptrace && t_0) {
                 for (const Mark &m : marks) {
                     float ms = 0.f;
@@ -1103,6 +1116,7 @@ static fm_status stats_impl(const Plan *p, uint64_t seed, int64_t first_sample, 
                             uint64_t *deg_plus, uint64_t *deg_minus, uint64_t *str_plus, uint64_t *str_minus,
                             uint64_t *rank_hist, fm_counters *out)
 {
+    NvtxRange nvtx_("fm_sample statistics mode (NEXT-3)");
     int64_t n_tasks = 0;
     const int64_t kf = std::min(tail_samples(p, 0), n_samples);
     const int64_t km = p->n_chunks[2] > 0 ? std::max<int64_t>(0, std::min(tail_samples(p, 2), n_samples) - kf) : 0;
@@ -1184,6 +1198,7 @@ fm_status fm_sample_ecm_ex(const fm_plan *plan, uint64_t seed, int64_t first_sam
 
 fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host, void *cuda_stream)
 {
+    NvtxRange nvtx_("fm_edges_to_host");
     if (!e) return fail(FM_ERR_INVALID, "NULL result");
     {
         std::lock_guard<std::mutex> lk(g_mu);

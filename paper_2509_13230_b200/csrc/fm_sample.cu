@@ -1149,15 +1149,19 @@ __global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : k
                     int64_t t = A.task_list ? A.task_list[my] : my;
                     // the task's range record from the block's shared-memory table (one LDS per
                     // field: selecting among the three ranges' parameters cost ~40 instructions)
-                    if (A.il_s[0] > 0 && !A.task_list) {  // chunk-major queue -> canonical task index
-                        const RangeRec &Q = s_rng[task_range(A.tm, my)];
-                        int64_t cq, sq;  // m = cq ns + sq (fp64 quotient estimate: no 64-bit division)
-                        divmod_est(my - Q.t0, Q.il_s, Q.inv_il, cq, sq);
-                        t = Q.t0 + sq * Q.n_chunks + cq;
-                    }
+                    // (queue index and task index lie in the same range: the chunk-major order permutes
+                    // the tasks of each range among themselves)
                     const RangeRec &Q = s_rng[task_range(A.tm, t)];
                     int64_t s, ch;
-                    divmod_est(t - Q.t0, Q.n_chunks, Q.inv_chunks, s, ch);
+                    if (A.il_s[0] > 0 && !A.task_list) {
+                        // chunk-major queue: position m of the range = chunk ch of its sample s
+                        // (m = ch ns + s; fp64 quotient estimate, no 64-bit division); canonical task
+                        // index t = t0 + s n_chunks + ch
+                        divmod_est(my - Q.t0, Q.il_s, Q.inv_il, ch, s);
+                        t = Q.t0 + s * Q.n_chunks + ch;
+                    } else {
+                        divmod_est(t - Q.t0, Q.n_chunks, Q.inv_chunks, s, ch);
+                    }
                     s += Q.s0;
                     const int64_t *seg_k = Q.seg, *cap_k = Q.cap;
                     s_task[ci] = t;

@@ -66,6 +66,23 @@ def main():
         fm.sample_degrees(p3, 3, n_samples=1)
         e3.free()
         p3.free()
+    # round 2: pipelined sample groups (two streams, TMA-staged compaction) and the big lane-chunks
+    xg, yg = WL.random_fitness(21, 6000, 2.4, 0.03, ecm=True)
+    for yy in (None, yg):
+        og = O.sample(O.sort_plan(xg, yy, seg_target=32), 8, n_samples=5)
+        for env in ({"FM_SAMPLE_GROUPS": "2", "FM_COMPACT_SMALL": "2"},
+                    {"FM_CHUNK_BIG_DRAWS": "300", "FM_TAIL_FACTOR_BIG": "0", "FM_TAIL_FACTOR": "0"}):
+            os.environ.update(env)
+            pg = fm.sort_plan(torch.from_numpy(xg).cuda(), None if yy is None else torch.from_numpy(yy).cuda(),
+                              seg_target=32)
+            eg = (fm.sample_ubcm if yy is None else fm.sample_ecm)(pg, 8, n_samples=5)
+            for k in env:
+                del os.environ[k]
+            assert np.array_equal(eg.edges.cpu().numpy(), og.edges), "groups/chunks"
+            if yy is not None:
+                assert np.array_equal(eg.weights.cpu().numpy(), og.weights), "groups/chunks weights"
+            eg.free()
+            pg.free()
     torch.cuda.synchronize()
     print("sanitize_run ok", d[-1], int(rc[0][-1]))
 

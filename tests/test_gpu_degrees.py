@@ -29,7 +29,7 @@ def edge_sums(e, n1, n2, bip):
 
 @pytest.mark.parametrize("ecm", [False, True])
 @pytest.mark.parametrize("kind", ["undirected", "bipartite", "directed"])
-def test_degrees_equal_edge_list_sums(kind, ecm):
+def test_degrees_equal_edge_list_sums(O, kind, ecm):
     n1 = 20_000
     n2 = 15_000 if kind == "bipartite" else n1
     x1, y1 = WL.random_fitness(5, n1, 2.3, 0.01, ecm=ecm)
@@ -51,6 +51,27 @@ def test_degrees_equal_edge_list_sums(kind, ecm):
         assert torch.equal(sp, q1)
         if kind != "undirected":
             assert torch.equal(sm, q2)
+    # ... and to the sums over the ORACLE's samples of the same seeds (not only the GPU's own lists)
+    okind = {"undirected": O.UNDIRECTED, "bipartite": O.BIPARTITE, "directed": O.DIRECTED}[kind]
+    if kind == "undirected":
+        op = O.sort_plan(x1, y1, seg_target=64)
+    else:
+        op = O.sort_plan(x1, y1, seg_target=64, kind=okind, x2=x2, y2=y2)
+    ref = O.sample(op, 9, n_samples=6, first_sample=4, nthreads=O.ncores())
+    oe = ref.edges.astype(np.int64)
+    o1, o2 = np.bincount(oe[:, 0], minlength=n1), np.bincount(oe[:, 1], minlength=n2)
+    if kind == "undirected":
+        assert np.array_equal(dp.cpu().numpy(), o1 + o2)
+    else:
+        assert np.array_equal(dp.cpu().numpy(), o1) and np.array_equal(dm.cpu().numpy(), o2)
+    if ecm:
+        ow = ref.weights.astype(np.int64)
+        w1 = np.bincount(oe[:, 0], weights=ow, minlength=n1).round().astype(np.int64)
+        w2 = np.bincount(oe[:, 1], weights=ow, minlength=n2).round().astype(np.int64)
+        if kind == "undirected":
+            assert np.array_equal(sp.cpu().numpy(), w1 + w2)
+        else:
+            assert np.array_equal(sp.cpu().numpy(), w1) and np.array_equal(sm.cpu().numpy(), w2)
 
 
 def test_config5_degree_gate_without_edge_lists(O):

@@ -13,7 +13,7 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden", "model_examples.txt")
 def test_model_examples_closed_form(O):
     """SPEC S:L80-84, S:L92, S:L122 examples (Eq. 4) via the oracle closed forms on N=2."""
     for line in open(GOLD):
-        if line.startswith("#") or not line.strip():
+        if line.startswith("#") or not line.strip() or line.startswith("pmf"):
             continue
         model, xi, xj, yi, yj, p, ew = line.split()
         x = np.array([float(xi), float(xj)])
@@ -23,6 +23,24 @@ def test_model_examples_closed_form(O):
         assert kv[0] == pytest.approx(float(p) * (1 - float(p)), abs=1e-15)
         if ew != "-":
             assert s[0] == pytest.approx(float(ew), abs=1e-12)
+
+
+def test_weight_pmf_examples(O):
+    """SPEC S:L102-103 (Eq. 5): P(w = 1 | edge) = 0.5 and P(w = 3 | edge) = 0.125 at t = 1/2, on
+    the sampler's own weights: N = 2, x = (1, 1), y = (sqrt(1/2), sqrt(1/2)) (so p = 0.5),
+    200,000 samples; 5 sigma."""
+    rows = [ln.split() for ln in open(GOLD) if ln.startswith("pmf")]
+    assert len(rows) == 2
+    R = 200_000
+    for _, w, yi, yj, pw in rows:
+        x = np.array([1.0, 1.0])
+        y = np.array([float(yi), float(yj)])
+        r = O.sample(O.sort_plan(x, y), seed=77, n_samples=R)
+        m = len(r.weights)
+        assert abs(m - 0.5 * R) < 5 * np.sqrt(0.25 * R)  # p = 0.5 (S:L92)
+        q = float(pw)
+        hits = int(np.sum(r.weights == int(w)))
+        assert abs(hits - q * m) < 5 * np.sqrt(q * (1 - q) * m), (w, hits, m)
 
 
 def test_weight_moments_closed_form(O):
