@@ -287,7 +287,7 @@ static fm_status sort_node_set(int model, int64_t n, const double *x, const doub
     CK(tmp.get(&work, tb), "alloc sort tmp");
     uint64_t *skeys;
     int32_t *perm;
-    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, ~0ull /* all 8 digit passes; a constant digit is a stable copy */, hist,
+    CK(radix_sort_u64_i32(ka, kb, ia, ib, n, ~0ull /* all 8 digit passes are launched; a constant digit's pass degenerates to a copy on the device */, hist,
                           &skeys, &perm, work, tb, st),
        "radix sort");
     tmp.release(perm);

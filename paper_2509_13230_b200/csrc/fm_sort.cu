@@ -2,8 +2,8 @@
 //
 // The sort key is ~bits(kappa): kappa >= 0 doubles order like their bit patterns, so sorting
 // the complement ascending gives kappa descending, and stability keeps ties in ascending id
-// (R9; P:L133 step (i), Alg. 1 line 3).  8-bit digits; a digit none of whose bits
-// varies across the keys is skipped.
+// (R9; P:L133 step (i), Alg. 1 line 3).  8-bit digits; a digit that is the same in every
+// key (seen in the up-front histograms, on the device) turns its pass into a plain copy.
 //
 // Launches: one memset of the look-back status, then ONE kernel per digit pass (the digit
 // histograms of all positions come with the keys from k_validate_key).  A pass kernel takes tiles in ticket order (atomic counter),
@@ -22,6 +22,10 @@ constexpr int kThreads = 256;
 #define FM_SORT_ITEMS 8
 #endif
 constexpr int kItems = FM_SORT_ITEMS;
+#ifndef FM_SORT_LB
+#define FM_SORT_LB 8
+#endif
+constexpr int kLB = FM_SORT_LB;  // predecessor tiles read per look-back step
 constexpr int kTile = kThreads * kItems;  // 2048 keys per tile, 256 per warp
 constexpr int kRadix = 256;
 constexpr int kPasses = 8;
@@ -48,10 +52,25 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     __shared__ uint64_t s_key[kTile];    // the tile in digit order (stable): coalesced global writes
     __shared__ int32_t s_val[kTile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned int hv = hist[threadIdx.x], inc = hv;
+    // a digit no key varies in (one bin holds all n keys, known from the up-front histograms without
+    // a host round trip): the pass is a stable identity -- a plain coalesced copy of the tile, no
+    // ranking, no look-back (e.g. the sign / high exponent byte when every kappa < 2)
+    if (__syncthreads_or(hv == (unsigned int)n)) {
+        const int64_t t0 = (int64_t)blockIdx.x * kTile;
+#pragma unroll
+        for (int r = 0; r < kItems; r++) {
+            const int64_t i = t0 + r * kThreads + threadIdx.x;
+            if (i < n) {
+                kout[i] = __ldcs(kin + i);
+                vout[i] = __ldcs(vin + i);
+            }
+        }
+        return;
+    }
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int w = 0; w < kThreads / 32; w++) wcnt[w][threadIdx.x] = 0;
     // exclusive scan of the pass's global digit counts: the base of each digit
-    unsigned int hv = hist[threadIdx.x], inc = hv;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
@@ -106,14 +125,14 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
             *(volatile uint64_t *)my = kFlagInc | cnt;
         } else {
             *(volatile uint64_t *)my = kFlagAgg | cnt;
-            // look back 8 predecessor tiles at a time (independent loads in flight)
-            for (int64_t j = tile - 1; j >= 0; j -= 8) {
-                uint64_t v[8];
+            // look back kLB predecessor tiles at a time (independent loads in flight)
+            for (int64_t j = tile - 1; j >= 0; j -= kLB) {
+                uint64_t v[kLB];
 #pragma unroll
-                for (int k = 0; k < 8; k++) v[k] = j - k >= 0 ? ld_volatile_u64(status + (j - k) * kRadix + d) : kFlagInc;
+                for (int k = 0; k < kLB; k++) v[k] = j - k >= 0 ? ld_volatile_u64(status + (j - k) * kRadix + d) : kFlagInc;
                 bool done = false;
 #pragma unroll
-                for (int k = 0; k < 8; k++) {
+                for (int k = 0; k < kLB; k++) {
                     if (done) break;
                     while ((v[k] & ~kValMask) == 0) v[k] = ld_volatile_u64(status + (j - k) * kRadix + d);
                     prefix += v[k] & kValMask;
