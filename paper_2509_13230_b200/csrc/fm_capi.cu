@@ -812,11 +812,15 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             // -2.2 % on config 4, -1.9 % on config 5; +1 % (UBCM) / +2.6 % (ECM) at N = 1e5, where
             // the records stay in L2 anyway: off there).  Results do not depend on it.
             // (the fused copy needs batches of consecutive canonical tasks: sample-major queue)
+            // chunk-major in the fine range at every N (FM_INTERLEAVE_FINE=0: off), so the last
+            // samples' hub-row chunks (sequential chains of up to S draws) start before their light rows
             a.il_s[0] = a.il_s[1] = a.il_s[2] = 0;
-            if (!fuse && p->nc >= env_i64("FM_INTERLEAVE_MIN", int64_t(1) << 19)) {
+            if (!fuse) {
+                const bool all = p->nc >= env_i64("FM_INTERLEAVE_MIN", int64_t(1) << 19);
+                const bool fine = env_i64("FM_INTERLEAVE_FINE", 1) != 0;
                 for (int r = 0; r < kRanges; r++) {
-                    a.il_s[r] = (r + 1 < kRanges ? q.tm.s0[r + 1] : q.R) - q.tm.s0[r];
-                    if (a.il_s[r] == 0) a.il_s[r] = 1;  // empty range: never indexed
+                    if (!all && !(fine && r == 2)) continue;
+                    a.il_s[r] = (r + 1 < kRanges ? q.tm.s0[r + 1] : q.R) - q.tm.s0[r];  // (0: empty range, never indexed)
                 }
             }
             a.tm = q.tm;

@@ -368,141 +368,6 @@ __device__ __forceinline__ void bulk_s2g(void *dst, uint32_t src_smem, unsigned 
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-
-constexpr int kStageBytes = 16384;  // the copier's staging buffer (shared memory, BlockRing::stage)
-
-// Copy the finished batch b to the final list at `prefix` through the staging buffer with bulk
-// copies: per round, the lanes of the tasks that fit load their slot (+ spill) into the stage at
-// 16-byte-aligned offsets (one cp.async.bulk each, completing on the mbarrier); then tasks whose
-// final position is 16-byte aligned are stored by one bulk store each, the others by the warp
-// (pairs re-aligned through shared memory).  Writes each task's final offset.  Warp-synchronous.
-__device__ __forceinline__ void batch_copy_tma(const SampleArgs &A, int64_t b, int64_t prefix, int64_t agg, int kb,
-                                               uint32_t stage, uint32_t mbar, unsigned &phase)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t T = A.n_tasks;
-    const int64_t t0 = b * kb, t1 = min(T, t0 + kb);
-    if (t1 == T && lane == 0) A.dest[T] = prefix + agg;
-    const char *base = reinterpret_cast<const char *>(A.edges);
-    int64_t run = prefix;
-    for (int64_t tb = t0; tb < t1; tb += 32) {
-        const int64_t t = tb + lane;
-        int64_t cnt = 0, src = 0, sp = -1, cap = 0;
-        if (t < t1) {
-            int64_t s_, c_;
-            int k_;
-            task_decode(A.tm, t, s_, c_, k_);
-            cap = FM_TM_SEL(A.tm, cap, k_)[c_ + 1] - FM_TM_SEL(A.tm, cap, k_)[c_];
-            src = s_ * A.tm.cap_per_sample + FM_TM_SEL(A.tm, cap, k_)[c_];
-            cnt = A.counts[t];
-            sp = A.spill_off[t];
-        }
-        int64_t incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const int64_t dst = run + incl - cnt;
-        if (t < t1) A.dest[t] = dst;
-        run += __shfl_sync(0xffffffffu, incl, 31);
-        const bool skip = (cnt > cap && (cnt > 2 * cap || sp < 0)) || dst + cnt > A.out_cap;
-        const int64_t ncp = skip ? 0 : cnt;
-        const int64_t n_slot = min(ncp, cap), n_sp = ncp - n_slot;
-        // staged bytes: the slot part (cap is a multiple of 4: a spilled slot part is whole 32-byte
-        // units) then the spill part, each rounded up to 16 bytes
-        const unsigned b_slot = (unsigned)(((n_slot + 1) & ~int64_t(1)) * 8);
-        const unsigned b_sp = (unsigned)(((n_sp + 1) & ~int64_t(1)) * 8);
-        const unsigned need = b_slot + b_sp;
-        // (a task larger than the stage -- only with very large seg_target -- is copied by the warp)
-        unsigned big = __ballot_sync(0xffffffffu, ncp > 0 && need > (unsigned)kStageBytes);
-        while (big) {
-            const int k = __ffs(big) - 1;
-            big &= big - 1;
-            const int64_t d_k = __shfl_sync(0xffffffffu, dst, k), c_k = __shfl_sync(0xffffffffu, ncp, k);
-            const int64_t s_k = __shfl_sync(0xffffffffu, src, k), p_k = __shfl_sync(0xffffffffu, sp, k);
-            const int64_t n_k = __shfl_sync(0xffffffffu, n_slot, k);
-            for (int64_t e = lane; e < c_k; e += 32)
-                __stcs(A.out_e + d_k + e, e < n_k ? A.edges[s_k + e] : A.spill_e[p_k + e - n_k]);
-        }
-        bool pending = ncp > 0 && need <= (unsigned)kStageBytes;
-        while (__any_sync(0xffffffffu, pending)) {
-            // this round: the pending tasks (in lane order) whose staging ranges fit
-            unsigned sz = pending ? need : 0u, inc = sz;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += v;
-            }
-            const unsigned off = inc - sz;
-            // the first pending task always fits (a task's slot + spill is < kStageBytes)
-            const bool mine = pending && inc <= (unsigned)kStageBytes;
-            const unsigned total = __reduce_add_sync(0xffffffffu, mine ? sz : 0u);
-            // (the stage's previous contents have been read: order the async-proxy writes after)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (lane == 0) mbar_arrive_expect(mbar, total);
-            __syncwarp();
-            if (mine) {
-                if (b_slot) bulk_g2s(stage + off, base + (size_t)src * 8, b_slot, mbar);
-                if (b_sp) bulk_g2s(stage + off + b_slot, A.spill_e + sp, b_sp, mbar);
-            }
-            mbar_wait(mbar, phase & 1);
-            phase++;
-            // the slot data is in shared memory: the scratch lines can be discarded (whole lines
-            // inside the slot only)
-            if (mine && A.discard && n_slot > 0) {
-                const size_t a = (size_t)src * 8, z = a + (size_t)cap * 8;
-                for (size_t l = (a + 127) & ~(size_t)127; l + 128 <= z; l += 128) discard_l2_line(base + l);
-            }
-            // aligned final position: one bulk store (the odd last element by the lane itself)
-            const bool even = (dst & 1) == 0;
-            if (mine && even) {
-                const unsigned nb = (unsigned)(ncp & ~int64_t(1)) * 8;
-                if (nb) bulk_s2g(A.out_e + dst, stage + off, nb);
-                if (ncp & 1) {
-                    // the element after the slot part's padding when spilled: staged contiguously
-                    // only if n_slot is even (spilled slot parts are multiples of 4), so index
-                    // ncp - 1 is at off + (ncp - 1) * 8 whenever n_sp == 0 or n_slot is even
-                    int2 e;
-                    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(stage + off + (unsigned)(ncp - 1) * 8));
-                    __stcs(A.out_e + dst + ncp - 1, e);
-                }
-            }
-            bulk_commit();
-            // odd final positions: the warp copies each such task, element 0 alone, then pairs
-            unsigned odd = __ballot_sync(0xffffffffu, mine && !even);
-            while (odd) {
-                const int k = __ffs(odd) - 1;
-                odd &= odd - 1;
-                const int64_t d_k = __shfl_sync(0xffffffffu, dst, k);
-                const int64_t c_k = __shfl_sync(0xffffffffu, ncp, k);
-                const unsigned o_k = __shfl_sync(0xffffffffu, off, k);
-                for (int64_t e0 = 2 * lane; e0 < c_k + 1; e0 += 64) {
-                    // output pair (d_k + e0 - 1, d_k + e0) for e0 >= 2 is 16-byte aligned; e0 = 0: element 0
-                    if (e0 == 0) {
-                        int2 e;
-                        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(stage + o_k));
-                        __stcs(A.out_e + d_k, e);
-                        continue;
-                    }
-                    int2 x0, x1 = make_int2(0, 0);
-                    asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(x0.x), "=r"(x0.y) : "r"(stage + o_k + (unsigned)(e0 - 1) * 8));
-                    if (e0 < c_k) {
-                        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(x1.x), "=r"(x1.y) : "r"(stage + o_k + (unsigned)e0 * 8));
-                        __stcs(reinterpret_cast<int4 *>(A.out_e + d_k + e0 - 1), make_int4(x0.x, x0.y, x1.x, x1.y));
-                    } else {
-                        __stcs(A.out_e + d_k + e0 - 1, x0);
-                    }
-                }
-            }
-            // the stage is re-filled next round: the bulk stores must have read it
-            bulk_wait_read();
-            __syncwarp();
-            pending = pending && !mine;
-        }
-    }
-}
 
 // ---- the pipelined copy: sub-batches of 32 tasks (one per lane) alternate between two staging
 // buffers, so the bulk loads of one sub-batch overlap the stores of the previous one ----
@@ -1153,7 +1018,7 @@ __global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : k
                     // the tasks of each range among themselves)
                     const RangeRec &Q = s_rng[task_range(A.tm, t)];
                     int64_t s, ch;
-                    if (A.il_s[0] > 0 && !A.task_list) {
+                    if (Q.il_s > 0 && !A.task_list) {
                         // chunk-major queue: position m of the range = chunk ch of its sample s
                         // (m = ch ns + s; fp64 quotient estimate, no 64-bit division); canonical task
                         // index t = t0 + s n_chunks + ch
@@ -1191,7 +1056,14 @@ __global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : k
 #pragma unroll
         for (int c = 0; c < kC; c++) any_act = any_act || act[c];
         if (!__any_sync(0xffffffffu, any_act)) {
-            if (warp_done) break;
+            // a task without segments (an empty last lane-chunk) fetched in this very round has not
+            // recorded its end yet (count, spill, batch bookkeeping happen at the lane's next fetch
+            // round): one more round before the warp leaves -- its counts were left unwritten when
+            // the queue ended with such tasks (found by tests/test_gpu_fuzz.py)
+            bool pend = false;
+#pragma unroll
+            for (int c = 0; c < kC; c++) pend = pend || s_task[threadIdx.x * kC + c] >= 0;
+            if (warp_done && !__any_sync(0xffffffffu, pend)) break;
             if (kFuse && fuse) {  // (ring full: the copier is behind)
                 __nanosleep(256);
             }

@@ -10,11 +10,6 @@ constexpr int kThreads = 256;
 constexpr int kItems = 8;
 constexpr int kTile = kThreads * kItems;
 
-struct SumI64 {
-    using T = int64_t;
-    __device__ static T id() { return 0; }
-    __device__ static T op(T a, T b) { return a + b; }
-};
 struct SumU64 {
     using T = uint64_t;
     __device__ static T id() { return 0; }

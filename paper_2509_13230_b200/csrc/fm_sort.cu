@@ -38,7 +38,20 @@ __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t *p)
     return v;
 }
 
-__global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
+__device__ __noinline__ void copy_tile(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
+                                       uint64_t *__restrict__ kout, int32_t *__restrict__ vout, int64_t n)
+{
+    const int64_t t0 = (int64_t)blockIdx.x * kTile;
+    for (int r = 0; r < kItems; r++) {
+        const int64_t i = t0 + r * kThreads + threadIdx.x;
+        if (i < n) {
+            kout[i] = __ldcs(kin + i);
+            vout[i] = __ldcs(vin + i);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_pass(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
                                                    uint64_t *__restrict__ kout, int32_t *__restrict__ vout, int64_t n,
                                                    int shift, const unsigned int *__restrict__ hist,
                                                    uint64_t *status, unsigned int *tile_counter)
@@ -52,22 +65,14 @@ __global__ void __launch_bounds__(kThreads) k_pass(const uint64_t *__restrict__ 
     __shared__ uint64_t s_key[kTile];    // the tile in digit order (stable): coalesced global writes
     __shared__ int32_t s_val[kTile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned int hv = hist[threadIdx.x], inc = hv;
     // a digit no key varies in (one bin holds all n keys, known from the up-front histograms without
     // a host round trip): the pass is a stable identity -- a plain coalesced copy of the tile, no
     // ranking, no look-back (e.g. the sign / high exponent byte when every kappa < 2)
-    if (__syncthreads_or(hv == (unsigned int)n)) {
-        const int64_t t0 = (int64_t)blockIdx.x * kTile;
-#pragma unroll
-        for (int r = 0; r < kItems; r++) {
-            const int64_t i = t0 + r * kThreads + threadIdx.x;
-            if (i < n) {
-                kout[i] = __ldcs(kin + i);
-                vout[i] = __ldcs(vin + i);
-            }
-        }
+    if (__syncthreads_or(hist[threadIdx.x] == (unsigned int)n)) {
+        copy_tile(kin, vin, kout, vout, n);  // (not inlined: the ranking path keeps its registers)
         return;
     }
+    unsigned int hv = hist[threadIdx.x], inc = hv;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int w = 0; w < kThreads / 32; w++) wcnt[w][threadIdx.x] = 0;
     // exclusive scan of the pass's global digit counts: the base of each digit

@@ -1,5 +1,7 @@
-# A/B of library variants on one box: python bench.py per variant, interleaved twice
+# A/B of library variants on one box: python bench.py per variant, interleaved twice.  VARIANTS="base x y", CFG
 mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for var in $VARIANTS; do [ "$var" = "base" ] || python paper_2509_13230_b200/build.py --variant $var $(eval echo \$DEF_$var) > gpurun_out/build_$var.log 2>&1; done
 CFG=${CFG:-5}
 for rep in 1 2; do
 for var in $VARIANTS; do

@@ -76,6 +76,18 @@ def test_plan_bit_identical(O, ecm, n, S):
     assert ulp.max(initial=0) <= 1  # CUDA log1p vs glibc log1p
 
 
+def test_plan_constant_radix_digit(O):
+    """Keys that agree in a whole radix digit (every kappa in [0.5, 2): the sign / high-exponent byte;
+    and x = j / 8: the low mantissa bytes): those passes are plain copies on the device; the
+    permutation is still the oracle's."""
+    rng = np.random.default_rng(5)
+    for x in (0.5 + 1.5 * rng.random(50_001) * (1 - 1e-12), np.arange(1, 40_000, dtype=np.float64) / 8.0):
+        x[7] = x[11]  # a tie
+        g = fm.sort_plan(torch.from_numpy(x).cuda(), seg_target=64).export()
+        o = O.sort_plan(x, seg_target=64)
+        assert np.array_equal(g["perm"], o.perm) and np.array_equal(g["kappa_s"], o.kappa_s)
+
+
 # ------------------------------------------------------------------------------ small cases
 @pytest.mark.parametrize("ecm", [False, True])
 @pytest.mark.parametrize("n,S,R", [(2, 256, 50), (5, 8, 200), (31, 8, 100), (1000, 8, 20), (4097, 256, 5),
@@ -291,3 +303,16 @@ def test_groups_with_overflow_rerun(monkeypatch):
     for s in range(6):
         a, b = e.offsets[s], e.offsets[s + 1]
         assert np.array_equal(key(E[a:b]), key(E2[a:b]))
+
+
+def test_queue_ending_with_empty_tasks(O):
+    """Regression (found by test_gpu_fuzz.py): an almost empty graph whose total work is just above a
+    multiple of the chunk target has an EMPTY last lane-chunk; in the chunk-major queue those tasks
+    are the last of the call, and the warps that fetched them used to leave before recording their
+    (zero) counts -- the scan then summed stale memory.  Dirty the pool first."""
+    xd, _ = WL.random_fitness(1, 50_000, 2.5, 0.05)
+    _ = gpu_run(xd, None, 256, 1, 8)  # leaves non-zero counts / offsets in the stream-ordered pool
+    x, _ = WL.random_fitness(58, 257, 2.5, 0.001)
+    for S in (37, 256):
+        for R in (13, 60, 64, 100):
+            check_parity(O, x, None, S, seed=342799134629, n_samples=R, first_sample=1, exact=True)
