@@ -673,8 +673,11 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     // copies the block's finished task batches into the final list.  Measured slower than the
     // compaction pass (the copier warp is issue-starved next to 23 sampler warps); one group only.
     const bool rank_out = model == FM_UBCM && p->nc >= env_i64("FM_UBCM_RANK_OUT_MIN", int64_t(1) << 21);
-    const bool fuse = model == FM_UBCM && p->slots_aligned && env_i64("FM_FUSE_WRITE", 0) != 0 &&
-                      (!rank_out || env_i64("FM_FUSE_RANKOUT", 0) != 0);
+    // (undirected plans only: the fused kernel is instantiated for (min id, max id) pairs; an ordered
+    // -- bipartite / directed -- plan with the option set used to skip the compaction and still
+    // launch the plain sampler: found by tests/test_gpu_fuzz.py)
+    const bool fuse = model == FM_UBCM && p->kind == FM_UNDIRECTED && p->slots_aligned &&
+                      env_i64("FM_FUSE_WRITE", 0) != 0 && (!rank_out || env_i64("FM_FUSE_RANKOUT", 0) != 0);
     // the small-footprint compaction needs 32-byte-aligned slots holding pairs (UBCM) or records
     // (ECM) and a warp's 32 tasks spanning < 2^31 output positions (slot <= ~1.25 (chunk + segment))
     const bool small_compact = buf4 && (model == FM_UBCM || ecm_rec) && (p->wmax >> kG) < (int64_t(1) << 22) &&

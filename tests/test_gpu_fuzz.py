@@ -23,6 +23,9 @@ OPTIONS = [
     {"FM_CHUNK_LANE_DRAWS": "16", "FM_CHUNK_FINE_DRAWS": "4", "FM_CHUNK_BIG_DRAWS": "40", "FM_TAIL_FACTOR_BIG": "0"},
     {"FM_UBCM_RANK_OUT_MIN": "0", "FM_INTERLEAVE_MIN": "0"},
     {"FM_INTERLEAVE_FINE": "0", "FM_SCRATCH_BUF4": "0"},
+    {"FM_FUSE_WRITE": "1"},                                   # (UBCM undirected only; ignored elsewhere)
+    {"FM_DEBUG_SCRATCH_CAP": "8", "FM_SAMPLE_GROUPS": "2"},   # slots overflow: spill regions and re-runs
+    {"FM_DEBUG_SCRATCH_CAP": "12"},
 ]
 
 
@@ -77,3 +80,89 @@ def test_fuzz_case(O, monkeypatch, i):
             assert np.array_equal(dp.cpu().numpy(), o1 + o2), c
         else:
             assert np.array_equal(dp.cpu().numpy(), o1) and np.array_equal(dm.cpu().numpy(), o2), c
+
+
+@pytest.mark.parametrize("i", range(36))
+def test_fuzz_medium(O, monkeypatch, i):
+    """The same sweep at N = 10,000 ... 60,000 (several blocks, many warp batches, hub rows cut into
+    segments), undirected and bipartite."""
+    r = np.random.default_rng(7000 + i)
+    ecm = bool(r.integers(2))
+    bip = bool(r.integers(3) == 0)
+    n1 = int(r.integers(10_000, 60_000))
+    n2 = int(r.integers(5_000, 30_000)) if bip else n1
+    gamma = float(r.choice([2.2, 2.5, 2.8]))
+    scale = float(r.choice([0.003, 0.01, 0.03]))
+    S = int(r.choice([8, 64, 256, 1000]))
+    R = int(r.choice([1, 3, 9]))
+    env = OPTIONS[(i * 5 + 3) % len(OPTIONS)]
+    seed = int(r.integers(1 << 50))
+    x1, y1 = WL.random_fitness(300 + i, n1, gamma, scale, ecm=ecm)
+    x2, y2 = WL.random_fitness(400 + i, n2, gamma, scale, ecm=ecm)
+    dev = lambda a: None if a is None else torch.from_numpy(a).cuda()  # noqa: E731
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    if bip:
+        plan = fm.sort_plan_bipartite(dev(x1), dev(x2), dev(y1), dev(y2), kind="bipartite", seg_target=S)
+        op = O.sort_plan(x1, y1, seg_target=S, kind="bipartite", x2=x2, y2=y2)
+    else:
+        plan = fm.sort_plan(dev(x1), dev(y1), seg_target=S)
+        op = O.sort_plan(x1, y1, seg_target=S)
+    e = (fm.sample_ecm if ecm else fm.sample_ubcm)(plan, seed, n_samples=R, first_sample=5)
+    ref = O.sample(op, seed, n_samples=R, first_sample=5, nthreads=O.ncores())
+    tag = dict(i=i, ecm=ecm, bip=bip, n1=n1, n2=n2, gamma=gamma, scale=scale, S=S, R=R, env=env)
+    assert np.array_equal(e.offsets, ref.offsets), tag
+    assert np.array_equal(e.edges.cpu().numpy().reshape(-1, 2), ref.edges.reshape(-1, 2)), tag
+    if ecm:
+        assert np.array_equal(e.weights.cpu().numpy(), ref.weights), tag
+    assert (e.draws, e.landed, e.accepted) == (ref.draws, ref.landed, ref.accepted), tag
+    if not bip and i % 2 == 0:  # rich-club profile of the same samples from the statistics mode
+        et, cnt = fm.sample_richclub(plan, seed, n_samples=R, first_sample=5)
+        want = O.richclub_count(op.perm, ref.edges.reshape(-1, 2))
+        assert np.array_equal(et.cpu().numpy().astype(np.int64), np.asarray(want).astype(np.int64)), tag
+
+
+def test_concurrent_host_threads(O, monkeypatch):
+    """Four host threads, each with its own stream, plan and seed, calling into the library at the
+    same time (ctypes releases the GIL): every result equals the oracle's.  Half of the threads
+    use pipelined sample groups (they share the device's side stream)."""
+    import threading
+
+    cases = []
+    for k in range(4):
+        x, y = WL.random_fitness(900 + k, 20_000 + 3_000 * k, 2.4, 0.02, ecm=True)
+        cases.append((x, y if k % 2 else None, 100 + k))
+    refs = [O.sample(O.sort_plan(x, y, seg_target=64), seed, n_samples=6, first_sample=k, nthreads=O.ncores())
+            for k, (x, y, seed) in enumerate(cases)]
+    monkeypatch.setenv("FM_SAMPLE_GROUPS", "2")
+    out, errs = [None] * 4, []
+
+    def work(k):
+        try:
+            x, y, seed = cases[k]
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                xd = torch.from_numpy(x).cuda()
+                yd = None if y is None else torch.from_numpy(y).cuda()
+                st.synchronize()
+                for _ in range(3):  # repeated: overlapping calls of different threads
+                    plan = fm.sort_plan(xd, yd, seg_target=64, stream=st)
+                    e = (fm.sample_ubcm if y is None else fm.sample_ecm)(plan, seed, n_samples=6, first_sample=k, stream=st)
+                    st.synchronize()
+                    out[k] = (e.offsets.copy(), e.edges.cpu().numpy().copy(),
+                              None if y is None else e.weights.cpu().numpy().copy())
+        except Exception as ex:  # noqa: BLE001
+            errs.append((k, repr(ex)))
+
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errs, errs
+    for k in range(4):
+        off, E, W = out[k]
+        assert np.array_equal(off, refs[k].offsets), k
+        assert np.array_equal(E.reshape(-1, 2), refs[k].edges.reshape(-1, 2)), k
+        if W is not None:
+            assert np.array_equal(W, refs[k].weights), k
