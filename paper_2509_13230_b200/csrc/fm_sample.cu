@@ -52,19 +52,28 @@ __device__ __forceinline__ unsigned smid()
 
 namespace {
 
+// block shape of the sampler: 24 warps per SM at <= 80 registers as 2 blocks of 384 threads (r02 A/B
+// against 3 x 256: config 5 -0.4 %, config 2 -1.6 %, ECM +-0: one log / range table and barrier
+// less per SM; 28 and 30 warps per SM -- 128 x 7, 224 x 4, 192 x 5 -- measured +0.3 ... +33 %)
 #ifndef FM_SAMPLE_THREADS
-#define FM_SAMPLE_THREADS 256
+#define FM_SAMPLE_THREADS 384
 #endif
 #ifndef FM_SAMPLE_MINB_UBCM
-#define FM_SAMPLE_MINB_UBCM 3
+#define FM_SAMPLE_MINB_UBCM 2
 #endif
 #ifndef FM_SAMPLE_MINB_ECM
-#define FM_SAMPLE_MINB_ECM 3
+#define FM_SAMPLE_MINB_ECM 2
+#endif
+#ifndef FM_SAMPLE_THREADS_RANKOUT  // the rank-out path keeps 4 x 256 threads at <= 64 registers
+#define FM_SAMPLE_THREADS_RANKOUT 256
 #endif
 #ifndef FM_SAMPLE_MINB_RANKOUT  // UBCM rank-out path (N >= 2^21: DRAM-latency-bound gathers)
 #define FM_SAMPLE_MINB_RANKOUT 4
 #endif
 constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
+constexpr int kThreadsRankOut = FM_SAMPLE_THREADS_RANKOUT;
+// block size of an instantiation: the fused write runs one block per SM, the rank-out path its own shape
+__host__ __device__ constexpr int sampler_threads(bool fuse, int gather) { return fuse ? 768 : gather == 2 ? kThreadsRankOut : kThreads; }
 constexpr int kBatch = kQueueBatch;  // tasks per warp batch
 
 // one sample range of the task map (TaskMap) for the sampler's shared-memory table
@@ -687,10 +696,10 @@ __device__ __forceinline__ void copier_loop(const SampleArgs &A, BlockRing &Rg, 
 // kFuse: v3 fused write (UBCM edge lists; the launch's a.fuse): the block's last warp is a copier.
 template <int kModel, int kMinBlocks, int kC, bool kStats, bool kRefresh, int kGather, bool kOrdered, bool kCheck,
           bool kFuse>
-__global__ void __launch_bounds__(kFuse ? kFuseThreads : kThreads, kFuse ? 1 : kMinBlocks) k_sample(const __grid_constant__ SampleArgs A)
+__global__ void __launch_bounds__(sampler_threads(kFuse, kGather), kFuse ? 1 : kMinBlocks) k_sample(const __grid_constant__ SampleArgs A)
 {
-    // block size: kThreads (several blocks per SM), or one fused block per SM
-    constexpr int kT = kFuse ? kFuseThreads : kThreads;
+    // block size: several blocks per SM, or one fused block per SM
+    constexpr int kT = sampler_threads(kFuse, kGather);
     extern __shared__ __align__(16) unsigned char s_dyn[];  // per-chain prefetch slots
     // rarely used per-chain task state lives in shared memory (registers are the occupancy limit)
     __shared__ int64_t s_task[kT * kC];   // current task id, -1 none
@@ -1820,7 +1829,7 @@ template <int kModel, int kMinB, int kC, bool kStats, bool kRefresh, int kGather
 static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
 {
     auto kern = k_sample<kModel, kMinB, kC, kStats, kRefresh, kGather, kOrdered, kCheck, kFuse>;
-    constexpr int kT = kFuse ? kFuseThreads : kThreads;
+    constexpr int kT = sampler_threads(kFuse, kGather);
     int dev = 0, sms = 0, per = 0;
     cudaError_t err = cudaGetDevice(&dev);
     if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
