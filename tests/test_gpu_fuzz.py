@@ -3,6 +3,8 @@ fitness scale x segmentation target x sample range x ECM bound refresh x schedul
 case element by element (offsets, edges in canonical order, weights, counters).  Small sizes: the
 sweep spans the degenerate regimes (empty rows, saturated hubs, one-segment and many-segment rows,
 tasks of a single draw) that the fixed-size tests only touch."""
+import os
+
 import numpy as np
 import pytest
 
@@ -45,7 +47,11 @@ def case(i):
                 env=OPTIONS[i % len(OPTIONS)], seed=int(r.integers(1 << 40)))
 
 
-@pytest.mark.parametrize("i", range(160))
+# FM_FUZZ_OFFSET / FM_FUZZ_N: run another (or a longer) slice of the sweep, e.g. to hunt for bugs ad hoc
+_OFF, _N = int(os.environ.get("FM_FUZZ_OFFSET", "0")), int(os.environ.get("FM_FUZZ_N", "160"))
+
+
+@pytest.mark.parametrize("i", range(_OFF, _OFF + _N))
 def test_fuzz_case(O, monkeypatch, i):
     c = case(i)
     x1, y1 = WL.random_fitness(50 + i, c["n1"], c["gamma"], c["scale"], ecm=c["ecm"])
@@ -82,7 +88,7 @@ def test_fuzz_case(O, monkeypatch, i):
             assert np.array_equal(dp.cpu().numpy(), o1) and np.array_equal(dm.cpu().numpy(), o2), c
 
 
-@pytest.mark.parametrize("i", range(36))
+@pytest.mark.parametrize("i", range(_OFF, _OFF + max(1, _N * 36 // 160)))
 def test_fuzz_medium(O, monkeypatch, i):
     """The same sweep at N = 10,000 ... 60,000 (several blocks, many warp batches, hub rows cut into
     segments), undirected and bipartite."""
