@@ -172,3 +172,76 @@ def test_concurrent_host_threads(O, monkeypatch):
         assert np.array_equal(E.reshape(-1, 2), refs[k].edges.reshape(-1, 2)), k
         if W is not None:
             assert np.array_equal(W, refs[k].weights), k
+
+
+# ------------------------------------------------------------------------------ API surface and extremes
+@pytest.mark.parametrize("i", range(24))
+def test_fuzz_api_surface(O, i):
+    """Host-pointer plans, fm_edges_to_host, ECM strength sums (all graph kinds), the T1 expectation
+    kernel on random nodes -- against the oracle on random small cases."""
+    r = np.random.default_rng(3000 + i)
+    ecm = bool(r.integers(2))
+    kind = ("undirected", "bipartite", "directed")[int(r.integers(3))]
+    n1 = int(r.choice([5, 40, 333, 2000]))
+    n2 = n1 if kind != "bipartite" else int(r.choice([3, 77, 900]))
+    scale = float(r.choice([0.02, 0.2, 1.0]))
+    S, R, seed = int(r.choice([8, 50, 256])), int(r.choice([1, 6, 40])), int(r.integers(1 << 30))
+    x1, y1 = WL.random_fitness(500 + i, n1, 2.5, scale, ecm=ecm)
+    x2, y2 = WL.random_fitness(600 + i, n2, 2.5, scale, ecm=ecm)
+    if kind == "undirected":
+        plan = fm.sort_plan(x1, y1, seg_target=S)  # host (numpy) inputs
+        op = O.sort_plan(x1, y1, seg_target=S)
+    else:
+        plan = fm.sort_plan_bipartite(x1, x2, y1, y2, kind=kind, seg_target=S)
+        op = O.sort_plan(x1, y1, seg_target=S, kind=kind, x2=x2, y2=y2)
+    e = (fm.sample_ecm if ecm else fm.sample_ubcm)(plan, seed, n_samples=R)
+    ref = O.sample(op, seed, n_samples=R, nthreads=O.ncores())
+    E, W = e.to_host()
+    assert np.array_equal(E.reshape(-1, 2), ref.edges.reshape(-1, 2))
+    if ecm:
+        assert np.array_equal(W, ref.weights)
+    dp, dm, sp, sm, cnt = fm.sample_degrees(plan, seed, n_samples=R)
+    oe = ref.edges.reshape(-1, 2).astype(np.int64)
+    ow = ref.weights.astype(np.int64) if ecm else np.ones(len(oe), np.int64)
+    d1, d2 = np.bincount(oe[:, 0], minlength=n1), np.bincount(oe[:, 1], minlength=n2)
+    s1 = np.bincount(oe[:, 0], weights=ow, minlength=n1).round().astype(np.int64)
+    s2 = np.bincount(oe[:, 1], weights=ow, minlength=n2).round().astype(np.int64)
+    if kind == "undirected":
+        assert np.array_equal(dp.cpu().numpy(), d1 + d2)
+        if ecm:
+            assert np.array_equal(sp.cpu().numpy(), s1 + s2)
+    else:
+        assert np.array_equal(dp.cpu().numpy(), d1) and np.array_equal(dm.cpu().numpy(), d2)
+        if ecm:
+            assert np.array_equal(sp.cpu().numpy(), s1) and np.array_equal(sm.cpu().numpy(), s2)
+    assert cnt["accepted"] == len(oe)
+    if kind == "undirected":  # T1: exact expectations of random nodes
+        nodes = r.choice(n1, size=min(n1, 50), replace=False).astype(np.int32)
+        k, kv, s, sv = fm.expected_degrees(x1, y1, nodes=nodes)
+        ok, okv, os_, osv = O.expected(x1, y1, nodes=nodes)
+        assert np.allclose(k.cpu().numpy(), ok, rtol=1e-12, atol=1e-300)
+        assert np.allclose(kv.cpu().numpy(), okv, rtol=1e-12, atol=1e-300)
+        if ecm:
+            assert np.allclose(s.cpu().numpy(), os_, rtol=1e-12) and np.allclose(sv.cpu().numpy(), osv, rtol=1e-11)
+
+
+def test_extremes(O):
+    """Many samples of tiny graphs (task counts far above the resident lanes), saturated and empty
+    fitness mixes, the largest admissible first_sample, S at both ends of its range."""
+    def same(x, y, S, seed, R, first=0):
+        plan = fm.sort_plan(torch.from_numpy(x).cuda(), None if y is None else torch.from_numpy(y).cuda(), seg_target=S)
+        e = (fm.sample_ubcm if y is None else fm.sample_ecm)(plan, seed, n_samples=R, first_sample=first)
+        ref = O.sample(O.sort_plan(x, y, seg_target=S), seed, n_samples=R, first_sample=first, nthreads=O.ncores())
+        assert np.array_equal(e.offsets, ref.offsets)
+        assert np.array_equal(e.edges.cpu().numpy().reshape(-1, 2), ref.edges.reshape(-1, 2))
+        if y is not None:
+            assert np.array_equal(e.weights.cpu().numpy(), ref.weights)
+        assert (e.draws, e.landed, e.accepted) == (ref.draws, ref.landed, ref.accepted)
+
+    same(np.array([0.7, 1.9]), None, 256, 1, 300_000)                      # N = 2, 3e5 samples
+    same(np.array([0.7, 1.9, 0.0]), np.array([0.5, 0.2, 0.3]), 8, 2, 100_000)  # N = 3 ECM, an isolated node
+    x = np.concatenate([np.full(40, 1e6), np.zeros(300), np.full(60, 1e-6)])   # saturated core, isolated, near-empty
+    same(x, None, 8, 3, 50)
+    same(x, np.full(len(x), 0.9), 1 << 40, 4, 20)                           # y close to 1: long weight tails; S = 2^40
+    xs, ys = WL.random_fitness(77, 3000, 2.2, 0.05, ecm=True)
+    same(xs, ys, 8, 5, 3, first=(1 << 32) - 3)                              # last admissible samples
