@@ -205,11 +205,32 @@ class Plan:
             pass
 
 
+class _EdgesOwner:
+    """Owns the library buffers of one fm_edges result and releases them when the last holder -- the
+    Edges object or a tensor view made from it -- goes away.  (The views must not keep the Edges
+    object itself alive: it caches them, and a cycle through a torch tensor is invisible to
+    Python's garbage collector -- every result whose .edges had been read used to leak.)"""
+
+    def __init__(self, st: _Edges):
+        self.st = st
+
+    def free(self):
+        if self.st is not None and self.st._owner:
+            lib.fm_free(C.byref(self.st))
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:  # pragma: no cover
+            pass
+
+
 class Edges:
     """Result of fm_sample_*: device edge list (+ weights), host offsets, counters."""
 
     def __init__(self, st: _Edges, stream):
         self._st = st
+        self._own = _EdgesOwner(st)
         self._stream = stream
         self.n_samples = st.n_samples
         self.n_edges = st.n_edges
@@ -225,7 +246,7 @@ class Edges:
         """torch.int32 [n_edges, 2] on the GPU (zero-copy view of library memory)."""
         if self._edges_t is None:
             import torch
-            self._edges_t = torch.as_tensor(_CAI(self._st.edges, (self.n_edges, 2), "<i4", self), device="cuda")
+            self._edges_t = torch.as_tensor(_CAI(self._st.edges, (self.n_edges, 2), "<i4", self._own), device="cuda")
         return self._edges_t
 
     @property
@@ -234,7 +255,7 @@ class Edges:
             return None
         if self._w_t is None:
             import torch
-            self._w_t = torch.as_tensor(_CAI(self._st.weights, (self.n_edges,), "<i4", self), device="cuda")
+            self._w_t = torch.as_tensor(_CAI(self._st.weights, (self.n_edges,), "<i4", self._own), device="cuda")
         return self._w_t
 
     def to_host(self, edges_out=None, weights_out=None, stream=None):
@@ -257,16 +278,10 @@ class Edges:
         return self.edges[a:b], (None if self.weights is None else self.weights[a:b])
 
     def free(self):
-        if self._st is not None and self._st._owner:
-            self._edges_t = None
-            self._w_t = None
-            lib.fm_free(C.byref(self._st))
-
-    def __del__(self):
-        try:
-            self.free()
-        except Exception:  # pragma: no cover
-            pass
+        """Release the device buffers now (views made from this result become invalid)."""
+        self._edges_t = None
+        self._w_t = None
+        self._own.free()
 
 
 def sort_plan(x, y=None, seg_target: int = 256, stream=None) -> Plan:

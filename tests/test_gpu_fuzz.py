@@ -245,3 +245,53 @@ def test_extremes(O):
     same(x, np.full(len(x), 0.9), 1 << 40, 4, 20)                           # y close to 1: long weight tails; S = 2^40
     xs, ys = WL.random_fitness(77, 3000, 2.2, 0.05, ecm=True)
     same(xs, ys, 8, 5, 3, first=(1 << 32) - 3)                              # last admissible samples
+
+
+def test_no_device_memory_leak():
+    """Plans, results and the tensor views of results are released by reference counting alone (the
+    views once kept their result alive in a cycle through a torch tensor, which Python's collector
+    cannot see: every result whose .edges had been read leaked); the library's own temporaries go
+    back to the pool.  300 plan + sample cycles over the graph kinds and scheduling options."""
+    import gc
+
+    def free_mib():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        fm.pool_trim(0)
+        return torch.cuda.mem_get_info()[0] / 2**20
+
+    x, y = WL.random_fitness(1, 30_000, 2.4, 0.02, ecm=True)
+    x2, y2 = WL.random_fitness(2, 11_000, 2.4, 0.02, ecm=True)
+    xd, yd, x2d, y2d = (torch.from_numpy(a).cuda() for a in (x, y, x2, y2))
+    envs = [{}, {"FM_SAMPLE_GROUPS": "3"}, {"FM_DEBUG_SCRATCH_CAP": "8"}, {"FM_FUSE_WRITE": "1"}]
+
+    def cycle(it):
+        env = envs[it % len(envs)]
+        os.environ.update(env)
+        try:
+            yy, yy2 = (yd, y2d) if it % 3 == 0 else (None, None)
+            if it % 4 == 1:
+                p = fm.sort_plan_bipartite(xd, x2d, yy, yy2, kind="bipartite", seg_target=64)
+            else:
+                p = fm.sort_plan(xd, yy, seg_target=64)
+            e = (fm.sample_ubcm if yy is None else fm.sample_ecm)(p, it, n_samples=3)
+            v = e.edges[:5].clone()  # a view of the result
+            w = e.weights
+            fm.sample_degrees(p, it, n_samples=1)
+            return int(v.sum().item()) + (0 if w is None else 1)
+        finally:
+            for k in env:
+                del os.environ[k]
+
+    gc.collect()
+    gc.disable()
+    try:
+        for it in range(12):  # every path once: lazily created streams, tables, module data
+            cycle(it)
+        f0 = free_mib()
+        for it in range(300):
+            cycle(it)
+        f1 = free_mib()
+    finally:
+        gc.enable()
+    assert f0 - f1 < 64, f"device memory: {f0:.0f} MiB free before, {f1:.0f} MiB after"
