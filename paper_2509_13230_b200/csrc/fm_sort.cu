@@ -6,27 +6,35 @@
 // key (seen in the up-front histograms, on the device) turns its pass into a plain copy.
 //
 // Launches: one memset of the look-back status, then ONE kernel per digit pass (the digit
-// histograms of all positions come with the keys from k_validate_key).  A pass kernel takes tiles in ticket order (atomic counter),
-// ranks its 2048 keys stably (warp __match_any_sync ranks + cross-warp prefix in shared
-// memory), publishes its per-digit counts and resolves its global offsets by decoupled
+// histograms of all positions come with the keys from k_validate_key).  A pass kernel takes tiles in
+// ticket order (atomic counter), ranks its 2048 (4096 from 2^20 keys) keys stably (warp
+// __match_any_sync ranks of all items first, then one counter update per item by the match's
+// leader lane + cross-warp prefix in shared memory), publishes its per-digit counts and resolves its global offsets by decoupled
 // look-back over the preceding tiles (64-bit status words: 2 flag bits + 62-bit count), stages
 // the tile in digit order in shared memory and writes each digit run contiguously (coalesced).
 // Each pass reads and writes the keys once (24 B per key).
+#include <cstdlib>
+#include <mutex>
+
 #include "fm_internal.cuh"
 
 namespace fm {
 namespace {
 
 constexpr int kThreads = 256;
-#ifndef FM_SORT_ITEMS
-#define FM_SORT_ITEMS 8
+#ifndef FM_SORT_ITEMS_BIG
+#define FM_SORT_ITEMS_BIG 16
 #endif
-constexpr int kItems = FM_SORT_ITEMS;
+#ifndef FM_SORT_BIG_MIN
+#define FM_SORT_BIG_MIN (1 << 20)
+#endif
+// keys per thread: 8 (tiles of 2048 keys) below FM_SORT_BIG_MIN keys, else 16 (tiles of 4096: half
+// the tiles, look-back chains and status traffic, twice the loads in flight per thread)
+constexpr int kItemsSmall = 8, kItemsBig = FM_SORT_ITEMS_BIG;
 #ifndef FM_SORT_LB
 #define FM_SORT_LB 8
 #endif
 constexpr int kLB = FM_SORT_LB;  // predecessor tiles read per look-back step
-constexpr int kTile = kThreads * kItems;  // 2048 keys per tile, 256 per warp
 constexpr int kRadix = 256;
 constexpr int kPasses = 8;
 constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
@@ -38,11 +46,12 @@ __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t *p)
     return v;
 }
 
+template <int kI>
 __device__ __noinline__ void copy_tile(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
                                        uint64_t *__restrict__ kout, int32_t *__restrict__ vout, int64_t n)
 {
-    const int64_t t0 = (int64_t)blockIdx.x * kTile;
-    for (int r = 0; r < kItems; r++) {
+    const int64_t t0 = (int64_t)blockIdx.x * (kThreads * kI);
+    for (int r = 0; r < kI; r++) {
         const int64_t i = t0 + r * kThreads + threadIdx.x;
         if (i < n) {
             kout[i] = __ldcs(kin + i);
@@ -51,25 +60,40 @@ __device__ __noinline__ void copy_tile(const uint64_t *__restrict__ kin, const i
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) k_pass(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
-                                                   uint64_t *__restrict__ kout, int32_t *__restrict__ vout, int64_t n,
-                                                   int shift, const unsigned int *__restrict__ hist,
-                                                   uint64_t *status, unsigned int *tile_counter)
+// dynamic shared memory of a pass block: the tile in digit order (keys, ids), the per-warp digit
+// counters, the per-digit global base and tile-local start
+template <int kI>
+constexpr size_t pass_smem_bytes()
 {
-    __shared__ int wcnt[kThreads / 32][kRadix];
-    __shared__ int64_t s_base[kRadix];   // global position of the tile's first key of each digit
-    __shared__ int s_lstart[kRadix];     // tile-local position of the tile's first key of each digit
+    return (size_t)kThreads * kI * (sizeof(uint64_t) + sizeof(int32_t)) + sizeof(int) * (kThreads / 32) * kRadix +
+           sizeof(int64_t) * kRadix + sizeof(int) * kRadix;
+}
+
+#ifndef FM_SORT_BIG_BLOCKS
+#define FM_SORT_BIG_BLOCKS 2
+#endif
+template <int kI>
+__global__ void __launch_bounds__(kThreads, kI > 8 ? FM_SORT_BIG_BLOCKS : 4)
+    k_pass(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+           int32_t *__restrict__ vout, int64_t n, int shift, const unsigned int *__restrict__ hist, uint64_t *status,
+           unsigned int *tile_counter)
+{
+    constexpr int kTile = kThreads * kI;
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(s_raw);             // the tile in digit order (stable): coalesced global writes
+    int64_t *s_base = reinterpret_cast<int64_t *>(s_key + kTile);      // global position of the tile's first key of each digit
+    int32_t *s_val = reinterpret_cast<int32_t *>(s_base + kRadix);
+    int(*wcnt)[kRadix] = reinterpret_cast<int(*)[kRadix]>(s_val + kTile);
+    int *s_lstart = reinterpret_cast<int *>(wcnt + kThreads / 32);      // tile-local position of the tile's first key of each digit
     __shared__ unsigned int s_wsum[kThreads / 32];
     __shared__ int s_wtot[kThreads / 32];
     __shared__ unsigned int s_tile;
-    __shared__ uint64_t s_key[kTile];    // the tile in digit order (stable): coalesced global writes
-    __shared__ int32_t s_val[kTile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // a digit no key varies in (one bin holds all n keys, known from the up-front histograms without
     // a host round trip): the pass is a stable identity -- a plain coalesced copy of the tile, no
     // ranking, no look-back (e.g. the sign / high exponent byte when every kappa < 2)
     if (__syncthreads_or(hist[threadIdx.x] == (unsigned int)n)) {
-        copy_tile(kin, vin, kout, vout, n);  // (not inlined: the ranking path keeps its registers)
+        copy_tile<kI>(kin, vin, kout, vout, n);  // (not inlined: the ranking path keeps its registers)
         return;
     }
     unsigned int hv = hist[threadIdx.x], inc = hv;
@@ -89,28 +113,54 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const uint64_t *__restrict
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t wbase = tile * kTile + (int64_t)wid * (kTile / (kThreads / 32));
     const int nvalid = (int)min((int64_t)kTile, n - tile * kTile);
-    uint64_t key[kItems];
-    int32_t val[kItems];
-    int dig[kItems], loc[kItems];
+    uint64_t key[kI];
+    int32_t val[kI];
+    int loc[kI];
     // all of the thread's loads issued before the first rank (the warp syncs below would
     // otherwise serialise one load latency per item)
 #pragma unroll
-    for (int r = 0; r < kItems; r++) {
+    for (int r = 0; r < kI; r++) {
         const int64_t i = wbase + r * 32 + lane;  // warp-contiguous, in input order
         const bool ok = i < n;
         key[r] = ok ? __ldcs(kin + i) : 0;
         val[r] = ok ? __ldcs(vin + i) : 0;
     }
+    // stable rank of each key among the warp's keys of the same digit.  Phase A: the peer masks of
+    // all items (independent warp matches, no shared memory); loc packs rank among the peers of the
+    // same item | leader lane << 8 | peer count << 16.  Phase B: per item, the leader bumps the
+    // warp's digit counter and broadcasts its old value (one LDS + STS by one lane, one shuffle).
 #pragma unroll
-    for (int r = 0; r < kItems; r++) {
+    for (int r = 0; r < kI; r++) {
         const bool ok = wbase + r * 32 + lane < n;
-        dig[r] = ok ? (int)((key[r] >> shift) & 0xFF) : kRadix;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
-        const int rank = __popc(peers & lt);
-        const int leader = __ffs(peers) - 1;
-        loc[r] = ok ? wcnt[wid][dig[r]] + rank : 0;
-        __syncwarp();
-        if (ok && lane == leader) wcnt[wid][dig[r]] += __popc(peers);
+        const int d = ok ? (int)((key[r] >> shift) & 0xFF) : kRadix;
+        // the lanes holding the same digit: nine ballots (one per digit bit and one for validity)
+        // instead of __match_any_sync -- MATCH.ANY measured as the pass's bottleneck on the B200
+        // (45 % of its stall samples sat on the 16 matches' results)
+        uint32_t peers = 0xffffffffu;
+#ifdef FM_SORT_MATCH
+        peers = __match_any_sync(0xffffffffu, d);
+#else
+#pragma unroll
+        for (int b = 0; b < 9; b++) {
+            const bool bit = (d >> b) & 1;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
+#endif
+        loc[r] = __popc(peers & lt) | ((__ffs(peers) - 1) << 8) | (__popc(peers) << 16);
+    }
+#pragma unroll
+    for (int r = 0; r < kI; r++) {
+        const bool ok = wbase + r * 32 + lane < n;
+        const int d = (int)((key[r] >> shift) & 0xFF);
+        const int leader = (loc[r] >> 8) & 0xFF;
+        int base = 0;
+        if (ok && lane == leader) {
+            base = wcnt[wid][d];
+            wcnt[wid][d] = base + (loc[r] >> 16);
+        }
+        base = __shfl_sync(0xffffffffu, base, leader);
+        loc[r] = ok ? base + (loc[r] & 0xFF) : -1;
         __syncwarp();
     }
     __syncthreads();
@@ -166,16 +216,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const uint64_t *__restrict
     __syncthreads();
     // stage the tile in digit order, then write it out contiguously per digit run
 #pragma unroll
-    for (int r = 0; r < kItems; r++) {
-        if (dig[r] < kRadix) {
-            const int p = s_lstart[dig[r]] + wcnt[wid][dig[r]] + loc[r];
+    for (int r = 0; r < kI; r++) {
+        if (loc[r] >= 0) {
+            const int d = (int)((key[r] >> shift) & 0xFF);
+            const int p = s_lstart[d] + wcnt[wid][d] + loc[r];
             s_key[p] = key[r];
             s_val[p] = val[r];
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kItems; r++) {
+    for (int r = 0; r < kI; r++) {
         const int p = r * kThreads + threadIdx.x;
         if (p < nvalid) {
             const uint64_t k = s_key[p];
@@ -187,11 +238,28 @@ __global__ void __launch_bounds__(kThreads, 4) k_pass(const uint64_t *__restrict
     }
 }
 
+template <int kI>
+cudaError_t launch_pass(const uint64_t *ki, const int32_t *vi, uint64_t *ko, int32_t *vo, int64_t n, int shift,
+                        const unsigned int *hist, uint64_t *status, unsigned int *tiles, cudaStream_t st)
+{
+    static std::once_flag once[kMaxDevices];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::call_once(once[dev], [] {
+        cudaFuncSetAttribute(k_pass<kI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes<kI>());
+    });
+    const int64_t nt = (n + kThreads * kI - 1) / (kThreads * kI);
+    k_pass<kI><<<(unsigned)nt, kThreads, pass_smem_bytes<kI>(), st>>>(ki, vi, ko, vo, n, shift, hist, status, tiles);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 size_t radix_tmp_bytes(int64_t n)
 {
-    const int64_t nt = (n + kTile - 1) / kTile;
+    const int64_t nt = (n + kThreads * kItemsSmall - 1) / (kThreads * kItemsSmall);  // (the smaller tile: an upper bound)
     return sizeof(uint64_t) * (size_t)(kPasses * nt * kRadix) + sizeof(unsigned int) * kPasses + 512;
 }
 
@@ -199,10 +267,15 @@ cudaError_t radix_sort_u64_i32(uint64_t *keys_a, uint64_t *keys_b, int32_t *vals
                                uint64_t vary_bits, const unsigned int *hist, uint64_t **key_out, int32_t **val_out,
                                void *tmp, size_t tmp_bytes, cudaStream_t st)
 {
-    const int64_t nt = (n + kTile - 1) / kTile;
+    // (FM_SORT_BIG_MIN in the environment: the key count from which the 4096-key tiles are used; tests)
+    const char *bm = getenv("FM_SORT_BIG_MIN");
+    const bool big = n >= (bm && *bm ? strtoll(bm, nullptr, 10) : (long long)FM_SORT_BIG_MIN);
+    const int64_t tile = kThreads * (big ? kItemsBig : kItemsSmall);
+    const int64_t nt = (n + tile - 1) / tile;
     if (tmp_bytes < radix_tmp_bytes(n)) return cudaErrorInvalidValue;
     uint64_t *status = (uint64_t *)tmp;
-    unsigned int *tiles = (unsigned int *)(status + kPasses * nt * kRadix);
+    const int64_t nt_max = (n + kThreads * kItemsSmall - 1) / (kThreads * kItemsSmall);
+    unsigned int *tiles = (unsigned int *)(status + kPasses * nt_max * kRadix);
     cudaError_t e = cudaMemsetAsync(tmp, 0, radix_tmp_bytes(n) - 512, st);
     if (e != cudaSuccess) return e;
     uint64_t *ki = keys_a, *ko = keys_b;
@@ -211,8 +284,10 @@ cudaError_t radix_sort_u64_i32(uint64_t *keys_a, uint64_t *keys_b, int32_t *vals
         const int shift = 8 * p;
         if (((vary_bits >> shift) & 0xFFull) == 0) continue;
         count_launch();
-        k_pass<<<(unsigned)nt, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist + p * kRadix,
-                                                  status + (int64_t)p * nt * kRadix, tiles + p);
+        uint64_t *stp = status + (int64_t)p * nt * kRadix;
+        e = big ? launch_pass<kItemsBig>(ki, vi, ko, vo, n, shift, hist + p * kRadix, stp, tiles + p, st)
+                : launch_pass<kItemsSmall>(ki, vi, ko, vo, n, shift, hist + p * kRadix, stp, tiles + p, st);
+        if (e != cudaSuccess) return e;
         uint64_t *tk = ki; ki = ko; ko = tk;
         int32_t *tv = vi; vi = vo; vo = tv;
     }

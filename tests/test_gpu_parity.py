@@ -76,6 +76,18 @@ def test_plan_bit_identical(O, ecm, n, S):
     assert ulp.max(initial=0) <= 1  # CUDA log1p vs glibc log1p
 
 
+@pytest.mark.parametrize("n", [5000, 4096 * 3, 100_003])
+def test_plan_sort_big_tiles(O, monkeypatch, n):
+    """The 4096-key radix tiles (used from 2^20 keys) forced at small n: ragged last tile, ties."""
+    monkeypatch.setenv("FM_SORT_BIG_MIN", "0")
+    x, y = WL.random_fitness(900 + n, n, 2.3, 0.01, ecm=True)
+    x[3] = x[9] = x[n - 1]
+    g = fm.sort_plan(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), seg_target=64).export()
+    o = O.sort_plan(x, y, seg_target=64)
+    assert np.array_equal(g["perm"], o.perm) and np.array_equal(g["kappa_s"], o.kappa_s)
+    assert np.array_equal(g["y_s"], o.y_s)
+
+
 def test_plan_constant_radix_digit(O):
     """Keys that agree in a whole radix digit (every kappa in [0.5, 2): the sign / high-exponent byte;
     and x = j / 8: the low mantissa bytes): those passes are plain copies on the device; the
