@@ -164,40 +164,27 @@ __global__ void __launch_bounds__(kThreads, kI > 8 ? FM_SORT_BIG_BLOCKS : 4)
         __syncwarp();
     }
     __syncthreads();
-    // thread d: tile-local prefix over warps, the tile's count of digit d, and its global base
+    // thread d: tile-local prefix over warps and the tile's count of digit d; the count is published
+    // and the first look-back loads are issued BEFORE the tile is staged in shared memory, so the
+    // predecessors' status words travel while the block scans and stages (their latency was exposed)
     int acc = 0;
+    const int d_own = threadIdx.x;
+    uint64_t *const my = status + tile * kRadix + d_own;
+    uint64_t v[kLB];
     {
-        const int d = threadIdx.x;
         for (int w = 0; w < kThreads / 32; w++) {
-            const int c = wcnt[w][d];
-            wcnt[w][d] = acc;
+            const int c = wcnt[w][d_own];
+            wcnt[w][d_own] = acc;
             acc += c;
         }
-        const uint64_t cnt = (uint64_t)acc;
-        uint64_t *my = status + tile * kRadix + d;
-        uint64_t prefix = 0;
         if (tile == 0) {
-            *(volatile uint64_t *)my = kFlagInc | cnt;
+            *(volatile uint64_t *)my = kFlagInc | (uint64_t)acc;
         } else {
-            *(volatile uint64_t *)my = kFlagAgg | cnt;
-            // look back kLB predecessor tiles at a time (independent loads in flight)
-            for (int64_t j = tile - 1; j >= 0; j -= kLB) {
-                uint64_t v[kLB];
+            *(volatile uint64_t *)my = kFlagAgg | (uint64_t)acc;
 #pragma unroll
-                for (int k = 0; k < kLB; k++) v[k] = j - k >= 0 ? ld_volatile_u64(status + (j - k) * kRadix + d) : kFlagInc;
-                bool done = false;
-#pragma unroll
-                for (int k = 0; k < kLB; k++) {
-                    if (done) break;
-                    while ((v[k] & ~kValMask) == 0) v[k] = ld_volatile_u64(status + (j - k) * kRadix + d);
-                    prefix += v[k] & kValMask;
-                    done = (v[k] & ~kValMask) == kFlagInc;
-                }
-                if (done) break;
-            }
-            *(volatile uint64_t *)my = kFlagInc | (prefix + cnt);
+            for (int k = 0; k < kLB; k++)
+                v[k] = tile - 1 - k >= 0 ? ld_volatile_u64(status + (tile - 1 - k) * kRadix + d_own) : kFlagInc;
         }
-        s_base[d] = (int64_t)(dbase + prefix);
     }
     // tile-local exclusive scan of the digit counts (block-wide over the 256 digits)
     {
@@ -223,6 +210,28 @@ __global__ void __launch_bounds__(kThreads, kI > 8 ? FM_SORT_BIG_BLOCKS : 4)
             s_key[p] = key[r];
             s_val[p] = val[r];
         }
+    }
+    // finish the look-back: kLB predecessor tiles at a time (independent loads in flight)
+    {
+        uint64_t prefix = 0;
+        if (tile > 0) {
+            for (int64_t j = tile - 1;; j -= kLB) {
+                bool done = false;
+#pragma unroll
+                for (int k = 0; k < kLB; k++) {
+                    if (done) break;
+                    while ((v[k] & ~kValMask) == 0) v[k] = ld_volatile_u64(status + (j - k) * kRadix + d_own);
+                    prefix += v[k] & kValMask;
+                    done = (v[k] & ~kValMask) == kFlagInc;
+                }
+                if (done) break;
+#pragma unroll
+                for (int k = 0; k < kLB; k++)
+                    v[k] = j - kLB - k >= 0 ? ld_volatile_u64(status + (j - kLB - k) * kRadix + d_own) : kFlagInc;
+            }
+            *(volatile uint64_t *)my = kFlagInc | (prefix + (uint64_t)acc);
+        }
+        s_base[d_own] = (int64_t)(dbase + prefix);
     }
     __syncthreads();
 #pragma unroll
