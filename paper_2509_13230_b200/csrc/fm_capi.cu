@@ -663,16 +663,15 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     } og{own};
     if (!offsets_h) return fail(FM_ERR_NOMEM, "host offsets");
 
-    // ---- the call = G SAMPLE GROUPS, pipelined ----
+    // ---- the call = G SAMPLE GROUPS (default G = 1; FM_SAMPLE_GROUPS) ----
     // Group g (consecutive samples) runs sampler -> count scan -> offsets -> overflow list ->
-    // compaction on stream g & 1 (the caller's stream and one side stream): while the persistent
-    // sampler of group g + 1 fills the GPU, the small-footprint compaction of group g runs next to
-    // it on every SM (HBM is ~10 % busy under the sampler), and the sampler blocks of group g + 1
-    // take over the SMs as the blocks of group g run out of tasks (no end-of-launch tail between
-    // groups).  Only the last group's compaction is exposed.  Scratch slots are double-buffered
-    // over the groups (2/G of the per-call scratch).  The groups' edges are consecutive in the
-    // final list: group g's base is the device-side running total gbase[g].  Results do not depend
-    // on G.  One host synchronisation at the end of the call.
+    // compaction on stream g & 1 (the caller's stream and one side stream), so the small-footprint
+    // compaction of group g can run next to the persistent sampler of group g + 1 on every SM.
+    // Scratch slots are double-buffered over the groups (2/G of the per-call scratch).  The groups'
+    // edges are consecutive in the final list: group g's base is the device-side running total
+    // gbase[g].  Results do not depend on G.  One host synchronisation at the end of the call.
+    // (Measured: the overlap works, but every extra sampler launch pays its own end-of-launch tail
+    // and the sampler slows next to the compaction's traffic; one group is the fastest.)
     struct Hdr {
         unsigned long long counters[3];
         unsigned int flags;
@@ -705,9 +704,9 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     // group count: FM_SAMPLE_GROUPS (default 1).  Measured on the B200: the
     // co-resident compaction does hide under the next group's sampler, but every extra sampler
     // launch pays its own end-of-launch tail (~0.4 ms on config 5: a block stays resident until its
-    // slowest lane ends, so the next group's blocks cannot move in early) and the sampler loses the
-    // issue slots the compaction takes (+7 % per co-run group), so one group is the fastest on all
-    // five configs; the option stays for memory-bound callers (scratch is 2/G of the call's).
+    // slowest lane ends, so the next group's blocks cannot move in early) and the latency-bound
+    // sampler slows by ~1.5 ms per 12.8 GB of compaction traffic next to it, so one group is the
+    // fastest on all five configs; the option stays for callers short of memory (scratch is 2/G).
     int64_t G = 1;
     if (n_samples > 1 && small_compact && !fuse) {
         const int64_t forced = env_i64("FM_SAMPLE_GROUPS", 1);
