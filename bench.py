@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle work budget for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-api", choices=["to_host", "two_calls"], default="to_host",
+                    help="e2e leg: fm_sample_to_host (overlapped D2H) or fm_sample_* followed by fm_edges_to_host")
     ap.add_argument("--refresh", action="store_true",
                     help="ECM: per-candidate beta_min refresh (fm_sample_ecm_ex FM_SAMPLE_BETA_REFRESH, NEXT-4)")
     ap.add_argument("--selftest-dist", action="store_true",
@@ -376,12 +378,23 @@ def run_own(args):
             a, m, b = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             a.record()
             plan = fm.sort_plan(xh, yh, seg_target=args.seg_target)       # host pointers -> H2D inside
-            e = sample(plan, w.seed, n_samples=R, first_sample=first)
-            if e.n_edges > eh.shape[0]:
-                eh = torch.empty((e.n_edges, 2), dtype=torch.int32).pin_memory()
-                wh = torch.empty(e.n_edges, dtype=torch.int32).pin_memory() if y is not None else None
-            m.record()
-            e.to_host(eh, wh)                                                 # D2H of the result
+            if args.e2e_api == "to_host":
+                # fm_sample_to_host: each group of samples is copied to the host while the next ones
+                # are generated (the D2H of the list inside the call)
+                e = fm.sample_to_host(plan, w.seed, eh, wh, n_samples=R, first_sample=first,
+                                      refresh=args.refresh and y is not None)
+                m.record()
+                if e.flags & fm.FM_FLAG_HOST_TRUNCATED:  # (host buffers too small: plain copy of the device list)
+                    eh = torch.empty((e.n_edges, 2), dtype=torch.int32).pin_memory()
+                    wh = torch.empty(e.n_edges, dtype=torch.int32).pin_memory() if y is not None else None
+                    e.to_host(eh, wh)
+            else:
+                e = sample(plan, w.seed, n_samples=R, first_sample=first)
+                if e.n_edges > eh.shape[0]:
+                    eh = torch.empty((e.n_edges, 2), dtype=torch.int32).pin_memory()
+                    wh = torch.empty(e.n_edges, dtype=torch.int32).pin_memory() if y is not None else None
+                m.record()
+                e.to_host(eh, wh)                                             # D2H of the result
             b.record()
             b.synchronize()
             if k > 0:  # first iteration is a warm-up
@@ -396,7 +409,10 @@ def run_own(args):
         e2e = {"value": e_edges / (sum(e_ms) * 1e-3), "unit": "edges/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": statistics.mean(e_ms), "steps": len(e_ms),
                "host_buffers": "pinned", "phase_ms": e_phase,
-               "d2h_gbs": d2h / (e_phase["d2h"] * 1e-3) / 1e9 if e_phase["d2h"] > 0 else None}
+               "api": "fm_sort_plan(host x) + fm_sample_to_host (D2H of each sample group overlaps the next groups)"
+               if args.e2e_api == "to_host" else "fm_sort_plan(host x) + fm_sample_* + fm_edges_to_host",
+               "d2h_gbs": (d2h / (e_phase["d2h"] * 1e-3) / 1e9 if e_phase["d2h"] > 1e-3 else None) if args.e2e_api != "to_host"
+               else d2h / (statistics.mean(e_ms) * 1e-3) / 1e9}
 
     if rank != 0:
         if world > 1:

@@ -61,7 +61,8 @@ typedef enum { FM_UNDIRECTED = 0, FM_BIPARTITE = 1, FM_DIRECTED = 2 } fm_graph;
 
 enum {
     FM_FLAG_WEIGHT_SATURATED = 1u, /* an ECM weight exceeded INT32_MAX and was clamped (R8) */
-    FM_FLAG_SCRATCH_RERUN = 2u     /* some chunks overflowed their scratch and were re-run (same result) */
+    FM_FLAG_SCRATCH_RERUN = 2u,    /* some chunks overflowed their scratch and were re-run (same result) */
+    FM_FLAG_HOST_TRUNCATED = 4u    /* fm_sample_to_host: the host buffers were too small, nothing valid in them */
 };
 
 /* Opaque, immutable sampling plan: the sorted order (P:L133 step (i); Alg. 1 line 3), the
@@ -179,6 +180,20 @@ fm_status fm_sample_richclub(const fm_plan *plan, uint64_t seed, int64_t first_s
 fm_status fm_expected_degrees(fm_model model, int64_t n, const double *x, const double *y, const int32_t *nodes,
                               int64_t n_nodes, double *k, double *kvar, double *s, double *svar,
                               void *cuda_stream);
+
+/* fm_sample_ubcm / fm_sample_ecm(_ex) with the result ALSO delivered to caller-owned HOST buffers
+ * (the model is the plan's; flags as fm_sample_ecm_ex; Algorithm 1's edge list E):
+ * edges_host int32[2*host_cap], weights_host int32[host_cap] (ECM; may be NULL).  The call runs as
+ * groups of samples and copies each group's part of the list to the host while the next groups are
+ * still being sampled, so the device -> host transfer (the bound of the host path: 8 B per edge over
+ * PCIe) starts after the first group instead of after the whole call.  Use page-locked host memory
+ * for the copies to be asynchronous.  `out` is filled as by fm_sample_* (the device list stays
+ * valid until fm_free).  If the list holds more than host_cap edges, out->flags has
+ * FM_FLAG_HOST_TRUNCATED, the host buffers hold nothing valid, and fm_edges_to_host can be called
+ * with larger buffers.  Same results as fm_sample_*; synchronises the stream. */
+fm_status fm_sample_to_host(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples, uint32_t flags,
+                            void *cuda_stream, int32_t *edges_host, int32_t *weights_host, int64_t host_cap,
+                            fm_edges *out);
 
 /* Copy a result to caller-owned HOST buffers: edges_host int32[2*n_edges], weights_host
  * int32[n_edges] (may be NULL).  Stream-ordered; synchronises the stream. */

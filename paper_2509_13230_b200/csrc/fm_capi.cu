@@ -178,20 +178,20 @@ void configure_pool(int dev)
 
 // one non-blocking side stream per device for the pipelined sample groups (shared by concurrent
 // calls: they are ordered by events, sharing only costs overlap)
-cudaError_t side_stream(cudaStream_t *out)
+cudaError_t side_stream(cudaStream_t *out, int which = 0)  // 0: the groups' second stream, 1: D2H copies
 {
     static std::mutex mu;
-    static cudaStream_t side[kMaxDevices] = {};
+    static cudaStream_t side[kMaxDevices][2] = {};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> lk(mu);
-    if (!side[dev]) {
-        e = cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking);
+    if (!side[dev][which]) {
+        e = cudaStreamCreateWithFlags(&side[dev][which], cudaStreamNonBlocking);
         if (e != cudaSuccess) return e;
     }
-    *out = side[dev];
+    *out = side[dev][which];
     return cudaSuccess;
 }
 
@@ -626,8 +626,15 @@ static int64_t tail_samples(const Plan *p, int k)
 }
 
 
+// host destination of fm_sample_to_host: the final list is copied to the host group by group while
+// the later groups are still being sampled (cap: capacity in edges; w may be NULL)
+struct HostDst {
+    int32_t *e = nullptr, *w = nullptr;
+    int64_t cap = 0;
+};
+
 static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int64_t first_sample, int64_t n_samples,
-                             uint32_t flags, void *cuda_stream, fm_edges *out)
+                             uint32_t flags, void *cuda_stream, fm_edges *out, const HostDst *host = nullptr)
 {
     NvtxRange nvtx_(model == FM_UBCM ? "fm_sample_ubcm (a5-a6)" : "fm_sample_ecm (a5-a6)");
     if (!out) return fail(FM_ERR_INVALID, "out is NULL");
@@ -709,7 +716,15 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     // fastest on all five configs; the option stays for callers short of memory (scratch is 2/G).
     int64_t G = 1;
     if (n_samples > 1 && small_compact && !fuse) {
-        const int64_t forced = env_i64("FM_SAMPLE_GROUPS", 1);
+        // (a host destination: one group per ~2 GB of expected list, at most 8 -- the call is bound
+        // by the D2H copies (8 B per edge over PCIe, ~55 GB/s), which hide the groups' tails; below
+        // ~4 GB the overlap gains less than the groups cost: measured -10 % on configs 3 and 4)
+        int64_t hg = 1;
+        if (host && host->e) {
+            const double bytes = 8.0 * (double)std::max<int64_t>(1, p->est_draws - p->n_seg) * (double)n_samples;
+            hg = env_i64("FM_HOST_GROUPS", std::min<int64_t>(8, (int64_t)(bytes / 2e9)));
+        }
+        const int64_t forced = env_i64("FM_SAMPLE_GROUPS", std::max<int64_t>(1, hg));
         if (forced > 0) G = forced;
         G = std::min<int64_t>(G, n_samples);
     }
@@ -752,6 +767,36 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
         };
         if (G > 1) CK(side_stream(&side), "side stream");
         auto stream_of = [&](int64_t g) { return (g & 1) ? side : st; };
+        // host destination (fm_sample_*_host): a copy stream and pinned words for the groups' bases
+        const bool to_host = host && host->e;
+        cudaStream_t copy_st = st;
+        int64_t *pin = nullptr, *pin_dev = nullptr;
+        if (to_host) {
+            CK(side_stream(&copy_st, 1), "copy stream");
+            // (one small mapped allocation per host thread and device, kept: cudaHostAlloc /
+            // cudaFreeHost per call cost 15-200 ms next to gigabytes of page-locked user buffers)
+            struct PinWords {
+                int64_t *p = nullptr;
+                size_t n = 0;
+                int dev = -1;
+            };
+            thread_local PinWords pw;
+            int dev = 0;
+            CK(cudaGetDevice(&dev), "device");
+            if (pw.n < (size_t)G + 1 || pw.dev != dev) {
+                if (pw.p) cudaFreeHost(pw.p);
+                pw.p = nullptr;
+                pw.n = 0;
+                const size_t want = std::max<size_t>((size_t)G + 1, 64);
+                CK(cudaHostAlloc((void **)&pw.p, sizeof(int64_t) * want, cudaHostAllocMapped), "pinned words");
+                pw.n = want;
+                pw.dev = dev;
+            }
+            pin = pw.p;
+            CK(cudaHostGetDevicePointer((void **)&pin_dev, pin, 0), "mapped words");
+        }
+        std::vector<char> pin_empty((size_t)G, 0);
+        bool host_done = false;  // the list has been copied to the host destination completely
 
         // ---- device memory (all from the caller's stream, before the fork) ----
         const int64_t slots = max_R * p->cap_per_sample;
@@ -914,6 +959,9 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
             if (fuse) CK(cudaMemsetAsync(grp_state, 0, sizeof(unsigned long long) * n_batches, st), "memset batch states");
             const bool timing = g_timing.load();
             cudaEvent_t t_a = nullptr, t_b = nullptr, t_c = nullptr, ev_prev = nullptr;
+            std::vector<cudaEvent_t> ev_off((size_t)G, nullptr), ev_done((size_t)G, nullptr);
+            host_done = false;
+            if (to_host) pin[0] = 0;
             if (timing) {
                 CK(new_event(&t_a, true), "event");
                 CK(new_event(&t_b, true), "event");
@@ -960,14 +1008,21 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                        "scan counts");
                 // the group's base is the running total of the preceding groups (the other stream)
                 if (ev_prev) CK(cudaStreamWaitEvent(s, ev_prev, 0), "wait for the preceding group's total");
+                // (to_host: the group's end in the list also goes to a mapped page-locked word, for the
+                // host's copy of the group's range)
                 if (q.n_tasks > 0) {
-                    CK(launch_offsets(q.R, q.tm, q.dest, offs_d + q.s0, gbase + g, gbase + g + 1, s), "offsets");
+                    CK(launch_offsets(q.R, q.tm, q.dest, offs_d + q.s0, gbase + g, gbase + g + 1,
+                                      to_host ? pin_dev + g + 1 : nullptr, s),
+                       "offsets");
                 } else {
                     CK(cudaMemcpyAsync(gbase + g + 1, gbase + g, sizeof(int64_t), cudaMemcpyDeviceToDevice, s), "base");
+                    if (to_host) pin_empty[(size_t)g] = 1;  // (its end = its start: resolved on the host)
                 }
-                if (G > 1) {
+                if (G > 1 || to_host) {
                     CK(new_event(&ev_prev, false), "event");
                     CK(cudaEventRecord(ev_prev, s), "event record");
+                    ev_off[(size_t)g] = ev_prev;
+                    if (G == 1) ev_prev = nullptr;
                 }
                 if (q.n_tasks > 0)
                     CK(launch_overflow(q.n_tasks, q.tm, q.counts, q.spill_off, &hd[g].n_overflow, q.ovl, s),
@@ -977,6 +1032,41 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                 mark(g, "scanned", s);
                 if (!fuse) CK(compact_group(g, cap, s), "compact");
                 mark(g, "compacted", s);
+                if (to_host) {
+                    CK(new_event(&ev_done[(size_t)g], false), "event");
+                    CK(cudaEventRecord(ev_done[(size_t)g], s), "event record");
+                }
+            }
+            if (to_host) {
+                // every group is queued: copy each group's range of the list to the host as soon as
+                // it is compacted, while the later groups are sampled (the host learns the range
+                // from the pinned base words; ranges beyond the host capacity are not copied)
+                NvtxRange nvtx_c("fm_sample: D2H of finished groups");
+                bool all = true;
+                for (int64_t g = 0; g < G; g++) {
+                    CK(cudaEventSynchronize(ev_off[(size_t)g]), "wait for a group's base");
+                    if (pin_empty[(size_t)g]) pin[g + 1] = pin[g];
+                    const int64_t lo = pin[g], hi = ((volatile int64_t *)pin)[g + 1];
+                    if (hi > cap || hi > host->cap) {  // (list or host buffer too small: handled after the pass)
+                        all = false;
+                        break;
+                    }
+                    if (hi == lo) continue;
+                    CK(cudaStreamWaitEvent(copy_st, ev_done[(size_t)g], 0), "copy after compaction");
+                    CK(cudaMemcpyAsync(host->e + 2 * lo, (const int32_t *)own->edges + 2 * lo, sizeof(int32_t) * 2 * (hi - lo),
+                                       cudaMemcpyDeviceToHost, copy_st),
+                       "copy edges to the host");
+                    if (host->w && own->weights)
+                        CK(cudaMemcpyAsync(host->w + lo, (const int32_t *)own->weights + lo, sizeof(int32_t) * (hi - lo),
+                                           cudaMemcpyDeviceToHost, copy_st),
+                           "copy weights to the host");
+                    mark(g, "on host", copy_st);
+                }
+                cudaEvent_t ev;
+                CK(new_event(&ev, false), "event");
+                CK(cudaEventRecord(ev, copy_st), "event record");
+                CK(cudaStreamWaitEvent(st, ev, 0), "join copies");
+                host_done = all;
             }
             if (G > 1) {  // join
                 cudaEvent_t ev;
@@ -1058,9 +1148,23 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                 if (h[(size_t)g].n_overflow > 0) CK(rerun_group(g, out_cap), "rerun");
             CK(cudaStreamSynchronize(st), "sync (sample, rerun)");
         }
+        bool host_short = false;
+        if (to_host) {
+            if (total > host->cap) {
+                host_short = true;  // the device list stays valid: fm_edges_to_host with a larger buffer
+            } else if ((!host_done || n_overflow > 0) && total > 0) {
+                // (the list was redone or tasks were re-run into it after the groups' copies)
+                CK(cudaMemcpyAsync(host->e, own->edges, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost, st),
+                   "copy edges to the host");
+                if (host->w && own->weights)
+                    CK(cudaMemcpyAsync(host->w, own->weights, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st),
+                       "copy weights to the host");
+                CK(cudaStreamSynchronize(st), "sync (copy to the host)");
+            }
+        }
         out->n_edges = total;
         out->flags = ((hflags & kFlagWeightSat) ? FM_FLAG_WEIGHT_SATURATED : 0u) |
-                     (n_overflow ? FM_FLAG_SCRATCH_RERUN : 0u);
+                     (n_overflow ? FM_FLAG_SCRATCH_RERUN : 0u) | (host_short ? FM_FLAG_HOST_TRUNCATED : 0u);
     }
     out->n_samples = n_samples;
     out->offsets = offsets_h;
@@ -1220,6 +1324,23 @@ fm_status fm_sample_ecm_ex(const fm_plan *plan, uint64_t seed, int64_t first_sam
         return fail(FM_ERR_INVALID, "unknown fm_sample_ecm_ex flags 0x%x", flags);
     }
     return sample_impl(FM_ECM, plan, seed, first_sample, n_samples, flags, cuda_stream, out);
+}
+
+fm_status fm_sample_to_host(const fm_plan *plan, uint64_t seed, int64_t first_sample, int64_t n_samples, uint32_t flags,
+                            void *cuda_stream, int32_t *edges_host, int32_t *weights_host, int64_t host_cap,
+                            fm_edges *out)
+{
+    if (out) memset(out, 0, sizeof(*out));
+    if (!plan || !plan_live(plan)) return fail(FM_ERR_STATE, "not a live fm_plan");
+    const Plan *p = (const Plan *)plan;
+    if (flags & ~(uint32_t)FM_SAMPLE_BETA_REFRESH) return fail(FM_ERR_INVALID, "unknown fm_sample_to_host flags 0x%x", flags);
+    if (p->model == FM_UBCM && flags) return fail(FM_ERR_INVALID, "FM_SAMPLE_BETA_REFRESH: ECM plans only");
+    if (!edges_host || host_cap < 0) return fail(FM_ERR_INVALID, "edges_host is NULL or host_cap < 0");
+    HostDst hd;
+    hd.e = edges_host;
+    hd.w = p->model == FM_ECM ? weights_host : nullptr;
+    hd.cap = host_cap;
+    return sample_impl(p->model, plan, seed, first_sample, n_samples, flags, cuda_stream, out, &hd);
 }
 
 fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weights_host, void *cuda_stream)

@@ -178,8 +178,9 @@ cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, 
                            const int32_t *rank_map, int ordered, int ecm_rec, int small, const int64_t *out_base,
                            cudaStream_t st);
 // offsets[s] = *base_in + (first final position of sample s), s <= n_samples; *base_out = the running total
+// (base_out_host: optional mapped page-locked host word that receives the running total as well)
 cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets,
-                           const int64_t *base_in, int64_t *base_out, cudaStream_t st);
+                           const int64_t *base_in, int64_t *base_out, int64_t *base_out_host, cudaStream_t st);
 // out[i] += in[i], i < n (uint64)
 cudaError_t launch_add_u64(const uint64_t *in, uint64_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_debug_eval(int fn, int64_t n, const double *in, double *out, cudaStream_t st);

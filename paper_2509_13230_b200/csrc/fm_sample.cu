@@ -72,8 +72,9 @@ namespace {
 #endif
 constexpr int kThreads = FM_SAMPLE_THREADS;  // threads per block of the sampler
 constexpr int kThreadsRankOut = FM_SAMPLE_THREADS_RANKOUT;
+constexpr int kFuseThreadsC = 768;  // fused launch: one block per SM, 23 sampler warps + 1 copier (24 warps at 80 registers fill the register file)
 // block size of an instantiation: the fused write runs one block per SM, the rank-out path its own shape
-__host__ __device__ constexpr int sampler_threads(bool fuse, int gather) { return fuse ? 768 : gather == 2 ? kThreadsRankOut : kThreads; }
+__host__ __device__ constexpr int sampler_threads(bool fuse, int gather) { return fuse ? kFuseThreadsC : gather == 2 ? kThreadsRankOut : kThreads; }
 constexpr int kBatch = kQueueBatch;  // tasks per warp batch
 
 // one sample range of the task map (TaskMap) for the sampler's shared-memory table
@@ -130,7 +131,6 @@ __device__ __forceinline__ uint32_t load_logtab()
 // on unfinished batches, and those run on sampler warps that never wait.
 constexpr uint64_t kGrpAgg = 1ull << 62, kGrpInc = 2ull << 62, kGrpVal = (1ull << 62) - 1;
 constexpr int kBRing = 128;             // ring entries per block (one bit each in 64-bit masks)
-constexpr int kFuseThreads = 768;       // fused launch: one block per SM, 23 sampler warps + 1 copier (24 warps at 80 registers fill the register file: 6 per SMSP)
 constexpr int kPackShift = 40;          // packed batch counter: finished tasks << 40 | edges
 #ifndef FM_COPY_JOBS
 #define FM_COPY_JOBS 8
@@ -1699,7 +1699,7 @@ __global__ void __launch_bounds__(kC2Threads, 16) k_compact2(int64_t n_tasks, co
 // running total for the next group, base_next = base + dest[n_tasks]
 __global__ void __launch_bounds__(128, 16) k_offsets(int64_t n_samples, const TaskMap tm, const int64_t *__restrict__ dest,
                                                      int64_t *__restrict__ offsets, const int64_t *__restrict__ base_in,
-                                                     int64_t *base_out)
+                                                     int64_t *base_out, int64_t *base_out_host)
 {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s > n_samples) return;
@@ -1707,6 +1707,9 @@ __global__ void __launch_bounds__(128, 16) k_offsets(int64_t n_samples, const Ta
     const int64_t v = base + dest[sample_first_task(tm, s)];  // dest[n_tasks] is the group's total
     offsets[s] = v;
     if (s == n_samples && base_out) *base_out = v;
+    // (mapped page-locked host word: the host learns the group's end without a copy-engine transfer,
+    // which would queue behind the D2H copies of the preceding groups' edges)
+    if (s == n_samples && base_out_host) *(volatile int64_t *)base_out_host = v;
 }
 
 __global__ void k_add_u64(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, int64_t n)
@@ -1972,10 +1975,11 @@ cudaError_t launch_compact(int64_t out_cap, int64_t n_tasks, const TaskMap &tm, 
 }
 
 cudaError_t launch_offsets(int64_t n_samples, const TaskMap &tm, const int64_t *dest, int64_t *offsets,
-                           const int64_t *base_in, int64_t *base_out, cudaStream_t st)
+                           const int64_t *base_in, int64_t *base_out, int64_t *base_out_host, cudaStream_t st)
 {
     count_launch();
-    k_offsets<<<(unsigned)((n_samples + 1 + 127) / 128), 128, 0, st>>>(n_samples, tm, dest, offsets, base_in, base_out);
+    k_offsets<<<(unsigned)((n_samples + 1 + 127) / 128), 128, 0, st>>>(n_samples, tm, dest, offsets, base_in, base_out,
+                                                                      base_out_host);
     return cudaGetLastError();
 }
 

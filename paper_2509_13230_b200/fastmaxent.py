@@ -24,12 +24,12 @@ LIB_PATH = os.path.join(_HERE, "libfastmaxent.so" if not os.environ.get("FM_LIB_
 
 FM_UBCM, FM_ECM = 0, 1
 FM_OK, FM_ERR_INVALID, FM_ERR_NOMEM, FM_ERR_CUDA, FM_ERR_BOUND, FM_ERR_STATE = 0, -1, -2, -3, -4, -5
-FM_FLAG_WEIGHT_SATURATED, FM_FLAG_SCRATCH_RERUN = 1, 2
+FM_FLAG_WEIGHT_SATURATED, FM_FLAG_SCRATCH_RERUN, FM_FLAG_HOST_TRUNCATED = 1, 2, 4
 STATUS_NAMES = {0: "FM_OK", -1: "FM_ERR_INVALID", -2: "FM_ERR_NOMEM", -3: "FM_ERR_CUDA", -4: "FM_ERR_BOUND",
                 -5: "FM_ERR_STATE"}
 FM_UNDIRECTED, FM_BIPARTITE, FM_DIRECTED = 0, 1, 2
 _KINDS = {"undirected": FM_UNDIRECTED, "bipartite": FM_BIPARTITE, "directed": FM_DIRECTED}
-SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_sample_ecm_ex", "fm_edges_to_host", "fm_plan_get_info",
+SYMBOLS = ["fm_sort_plan", "fm_sort_plan_bipartite", "fm_plan_export_candidates", "fm_sample_degrees", "fm_sample_richclub", "fm_sample_ubcm", "fm_sample_ecm", "fm_sample_ecm_ex", "fm_edges_to_host", "fm_sample_to_host", "fm_plan_get_info",
            "fm_plan_export", "fm_free", "fm_last_error", "fm_abi_version", "fm_timing_enable", "fm_timing_get", "fm_debug_eval", "fm_expected_degrees",
            "fm_pool_trim"]
 
@@ -88,6 +88,8 @@ def _load():
     if hasattr(L, "fm_pool_trim") or not os.environ.get("FM_LIB_VARIANT"):
         L.fm_pool_trim.argtypes = [u64]
         L.fm_pool_trim.restype = C.c_int
+    L.fm_sample_to_host.argtypes = [vp, u64, i64, i64, C.c_uint32, vp, vp, vp, i64, C.POINTER(_Edges)]
+    L.fm_sample_to_host.restype = C.c_int
     L.fm_edges_to_host.argtypes = [C.POINTER(_Edges), vp, vp, vp]
     L.fm_edges_to_host.restype = C.c_int
     L.fm_plan_get_info.argtypes = [vp, C.POINTER(_PlanInfo)]
@@ -348,6 +350,32 @@ def sample_ecm(plan: Plan, seed: int, n_samples: int = 1, first_sample: int = 0,
     s = _stream(stream)
     _check(lib.fm_sample_ecm_ex(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
                                 FM_SAMPLE_BETA_REFRESH, s, C.byref(st)))
+    return Edges(st, s)
+
+
+def sample_to_host(plan: Plan, seed: int, edges_out, weights_out=None, n_samples: int = 1, first_sample: int = 0,
+                   stream=None, refresh: bool = False) -> Edges:
+    """fm_sample_to_host: sample like sample_ubcm / sample_ecm (the plan's model) and deliver the list
+    into caller-provided host buffers as well -- edges_out int32 [cap, 2], weights_out int32 [cap]
+    (numpy arrays or CPU torch tensors, ideally page-locked) -- copying each group of samples while
+    the next ones are generated.  Returns the Edges result (device list, offsets, counters);
+    result.flags & FM_FLAG_HOST_TRUNCATED: the host buffers were too small (nothing valid in them)."""
+    def ptr_cap(a, per):
+        if a is None:
+            return None, 0
+        if hasattr(a, "data_ptr"):
+            assert a.dtype.itemsize == 4 and a.is_contiguous() and not a.is_cuda
+            return C.c_void_p(a.data_ptr()), a.numel() // per
+        assert a.dtype == np.int32 and a.flags["C_CONTIGUOUS"]
+        return C.c_void_p(a.ctypes.data), a.size // per
+    ep, cap = ptr_cap(edges_out, 2)
+    wp, wcap = ptr_cap(weights_out, 1)
+    if wp is not None:
+        cap = min(cap, wcap)
+    st = _Edges()
+    s = _stream(stream)
+    _check(lib.fm_sample_to_host(plan._h, int(seed) & 0xFFFFFFFFFFFFFFFF, int(first_sample), int(n_samples),
+                                 FM_SAMPLE_BETA_REFRESH if refresh else 0, s, ep, wp, int(cap), C.byref(st)))
     return Edges(st, s)
 
 

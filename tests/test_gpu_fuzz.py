@@ -295,3 +295,39 @@ def test_no_device_memory_leak():
     finally:
         gc.enable()
     assert f0 - f1 < 64, f"device memory: {f0:.0f} MiB free before, {f1:.0f} MiB after"
+
+
+@pytest.mark.parametrize("ecm", [False, True])
+@pytest.mark.parametrize("env", [{}, {"FM_HOST_GROUPS": "3"}, {"FM_DEBUG_SCRATCH_CAP": "8"}, {"FM_HOST_GROUPS": "1"}])
+def test_sample_to_host(O, monkeypatch, ecm, env):
+    """fm_sample_to_host: the host buffers hold the oracle's list (copied group by group while later
+    groups are sampled), also after forced slot overflows (re-run tasks: copied again); too small
+    host buffers are reported, the device list stays valid."""
+    x, y = WL.random_fitness(41, 25_000, 2.4, 0.02, ecm=True)
+    yy = y if ecm else None
+    R = 11
+    ref = O.sample(O.sort_plan(x, yy, seg_target=64), 5, n_samples=R, first_sample=2, nthreads=O.ncores())
+    n_e = len(ref.edges.reshape(-1, 2))
+    plan = fm.sort_plan(torch.from_numpy(x).cuda(), None if yy is None else torch.from_numpy(yy).cuda(), seg_target=64)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    eh = torch.full((n_e + 100, 2), -7, dtype=torch.int32).pin_memory()
+    wh = torch.full((n_e + 100,), -7, dtype=torch.int32).pin_memory() if ecm else None
+    e = fm.sample_to_host(plan, 5, eh, wh, n_samples=R, first_sample=2)
+    assert not (e.flags & fm.FM_FLAG_HOST_TRUNCATED) and e.n_edges == n_e
+    assert np.array_equal(e.offsets, ref.offsets)
+    assert np.array_equal(eh.numpy()[:n_e], ref.edges.reshape(-1, 2))
+    assert np.all(eh.numpy()[n_e:] == -7)  # nothing written beyond the list
+    assert np.array_equal(e.edges.cpu().numpy(), ref.edges.reshape(-1, 2))  # the device list as well
+    if ecm:
+        assert np.array_equal(wh.numpy()[:n_e], ref.weights) and np.all(wh.numpy()[n_e:] == -7)
+    # pageable numpy destination, exact size
+    en = np.full((n_e, 2), -7, np.int32)
+    e2 = fm.sample_to_host(plan, 5, en, None, n_samples=R, first_sample=2)
+    assert np.array_equal(en, ref.edges.reshape(-1, 2)) and e2.n_edges == n_e
+    # too small: reported, buffers unspecified, fm_edges_to_host still works
+    small = np.full((n_e // 2, 2), -7, np.int32)
+    e3 = fm.sample_to_host(plan, 5, small, None, n_samples=R, first_sample=2)
+    assert e3.flags & fm.FM_FLAG_HOST_TRUNCATED and e3.n_edges == n_e
+    E3, _ = e3.to_host()
+    assert np.array_equal(E3, ref.edges.reshape(-1, 2))
