@@ -56,6 +56,8 @@ for it in range(8):
     e = (fm.sample_ubcm if it < 4 else fm.sample_ecm)(p, 1, n_samples=2)
     fm.sample_degrees(p, 1, n_samples=2)
     del e, p
+HOST_E = torch.empty((4_000_000, 2), dtype=torch.int32).pin_memory()
+HOST_W = torch.empty(4_000_000, dtype=torch.int32).pin_memory()
 f0 = free_mb()
 for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 200):
     env, yy = variants[it % len(variants)]
@@ -68,6 +70,11 @@ for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 200):
         fm.sample_richclub(p, it, n_samples=2)
     if it % 7 == 0:
         e.to_host()
+    if it % 6 == 1:  # the overlapped host path (forced groups)
+        os.environ["FM_HOST_GROUPS"] = "3"
+        eh = fm.sample_to_host(p, it, HOST_E, HOST_W if yy is not None else None, n_samples=4)
+        del os.environ["FM_HOST_GROUPS"]
+        del eh
     if it % 2 == 0:  # tensor views of the result (they once kept the result alive in an uncollectable cycle)
         v = e.edges[:10].clone()
         w = e.weights
