@@ -1855,8 +1855,11 @@ static cudaError_t launch_sample_t(const SampleArgs &a, cudaStream_t st)
         int carve = cv && *cv ? atoi(cv) : 40;
         cudaFuncAttributes fa;
         if (carve >= 0 && cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
-            // (+ one co-resident small-footprint compaction block of the pipelined sample groups)
-            const size_t need = (size_t)(kFuse ? 1 : kMinB) * (fa.sharedSizeBytes + dyn + 1024) + kC2Smem + 2048;
+            // (FM_SAMPLE_GROUPS set: + one co-resident small-footprint compaction block of the pipelined
+            // sample groups; the driver rounds the preference down as long as the sampler fits, so in
+            // practice only FM_SAMPLE_CARVEOUT=100 makes that room)
+            const size_t need = (size_t)(kFuse ? 1 : kMinB) * (fa.sharedSizeBytes + dyn + 1024) +
+                                (getenv("FM_SAMPLE_GROUPS") ? kC2Smem + 2048 : 0);
             const int pct = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
             carve = std::max(carve, std::min(pct, 100));
         }
