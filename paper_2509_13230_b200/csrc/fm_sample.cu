@@ -1133,7 +1133,7 @@ __global__ void __launch_bounds__(sampler_threads(kFuse, kGather), kFuse ? 1 : k
                         idd[c] = v1.y;
                         if (kRefresh) ymn[c] = __ldg(A.ymax_c + cur[c] + 1);
                     } else if (kGather == 2) {  // UBCM: κ only, the id is mapped in the compaction
-                        kv[c] = A.kappa_s[cur[c]];
+                        kv[c] = A.kappa_s[cur[c]];  // (ld.global.cg / .nc measured +-0 on config 4)
                     } else if (kGather == 1) {  // UBCM, large N: one 16-byte record (κ, π): one DRAM access
                         const double2 v0 = __ldg(A.cand + (uint32_t)cur[c]);
                         kv[c] = v0.x;
