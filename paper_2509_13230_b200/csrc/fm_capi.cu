@@ -617,7 +617,7 @@ static int64_t tail_samples(const Plan *p, int k)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const double lanes = (double)sms * 768.0;
-    // (big tasks: a warp claims 64 queue entries at a time, two long tasks per lane, so the work
+    // (big tasks: a warp claims a queue batch at a time -- 64 entries then: two long tasks per lane --, so the work
     // behind the big range must be larger: with factor 2 configs 3 and 4 lost 5-14 %; 3 against 4:
     // config 5 -0.45 %, config 4 -0.6 %, configs 2 and 3 unchanged)
     const int64_t factor = k == 2 ? env_i64("FM_TAIL_FACTOR_BIG", 3) : env_i64("FM_TAIL_FACTOR", 2);

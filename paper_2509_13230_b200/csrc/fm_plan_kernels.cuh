@@ -113,7 +113,14 @@ __device__ __forceinline__ void task_decode(const TaskMap &M, int64_t t, int64_t
 }
 
 // tasks per claim of the sampler's global queue (a warp batch; the fused write's unit)
-constexpr int kQueueBatch = 64;
+// 32 = one task per lane and claim, the minimum (a fetch round hands out up to 32 positions and
+// opens at most one new batch).  Against 64: config 5 sampler -0.75 %, config 2 -2.9 %, config 4
+// -3.3 % (the warps' last claims are smaller: shorter end of the queue); 128: +2.5 ... +44 %.
+#ifndef FM_QUEUE_BATCH
+#define FM_QUEUE_BATCH 32
+#endif
+constexpr int kQueueBatch = FM_QUEUE_BATCH;
+static_assert(kQueueBatch >= 32, "a fetch round serves up to 32 lanes from at most one new batch");
 
 struct SampleArgs {
     const unsigned char *rec;      // segment records, stride kRecStride(model)
