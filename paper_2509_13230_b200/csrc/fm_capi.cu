@@ -507,7 +507,7 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
 
     // ---- lane-chunking (never changes results): coarse, fine and big (FM_CHUNK_BIG_DRAWS=0: none) ----
     const int64_t total = h_sc.total_work;
-    const int64_t lane_draws[3] = {std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 128)),
+    const int64_t lane_draws[3] = {std::max<int64_t>(1, env_i64("FM_CHUNK_LANE_DRAWS", 256)),
                                    std::max<int64_t>(1, env_i64("FM_CHUNK_FINE_DRAWS", 64)),
                                    std::max<int64_t>(0, env_i64("FM_CHUNK_BIG_DRAWS", 512))};
     const int64_t cap_override = env_i64("FM_DEBUG_SCRATCH_CAP", 0);  // test hook: force re-runs
