@@ -151,39 +151,39 @@ constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ul
 
 // kT = 128 with <= 32 registers (kMinB = 16) is the small-footprint variant: one such block fits
 // next to three resident sampler blocks per SM (the pipelined sample groups).
-template <int kT, int kMinB>
+template <int kT, int kMinB, int kIt>
 __global__ void __launch_bounds__(kT, kMinB) k_scan_lb(const uint64_t *in, uint64_t *out, int64_t n,
                                                        uint64_t *status, unsigned int *ticket)
 {
-    constexpr int kTile = kT * kItems;
+    constexpr int kTile = kT * kIt;
     __shared__ unsigned int s_tile;
     __shared__ uint64_t s_prefix;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
-    const int64_t base = tile * kTile + (int64_t)threadIdx.x * kItems;
-    uint64_t v[kItems];
+    const int64_t base = tile * kTile + (int64_t)threadIdx.x * kIt;
+    uint64_t v[kIt];
     uint64_t acc = 0;
-    // a thread's 8 items are 64 contiguous bytes: 16-byte vector loads when the 8 are in range and
+    // a thread's kIt items are contiguous (64 or 128 bytes): 16-byte vector loads when the 8 are in range and
     // the array is 16-byte aligned (every caller's is)
-    const bool vec = base + kItems <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    const bool vec = base + kIt <= n && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
     if (vec) {
         const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(in + base);
 #pragma unroll
-        for (int k = 0; k < kItems / 2; k++) {
+        for (int k = 0; k < kIt / 2; k++) {
             const ulonglong2 w = q[k];
             v[2 * k] = w.x;
             v[2 * k + 1] = w.y;
         }
     } else {
 #pragma unroll
-        for (int k = 0; k < kItems; k++) {
+        for (int k = 0; k < kIt; k++) {
             const int64_t i = base + k;
             v[k] = i < n ? in[i] : 0;
         }
     }
 #pragma unroll
-    for (int k = 0; k < kItems; k++) acc += v[k];
+    for (int k = 0; k < kIt; k++) acc += v[k];
     uint64_t tot;
     const uint64_t exc = block_exclusive<SumU64, kT>(acc, &tot);
     if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kT, kMinB) k_scan_lb(const uint64_t *in, uint6
     if (vec) {
         ulonglong2 *q = reinterpret_cast<ulonglong2 *>(out + base);
 #pragma unroll
-        for (int k = 0; k < kItems / 2; k++) {
+        for (int k = 0; k < kIt / 2; k++) {
             const uint64_t a0 = pre;
             pre += v[2 * k];
             q[k] = make_ulonglong2(a0, pre);
@@ -226,19 +226,26 @@ __global__ void __launch_bounds__(kT, kMinB) k_scan_lb(const uint64_t *in, uint6
         }
     } else {
 #pragma unroll
-        for (int k = 0; k < kItems; k++) {
+        for (int k = 0; k < kIt; k++) {
             const int64_t i = base + k;
             if (i < n) out[i] = pre;
             pre += v[k];
         }
     }
-    if (tile == (n - 1) / kTile && threadIdx.x == ((n - 1) % kTile) / kItems) out[n] = pre;  // total
+    if (tile == (n - 1) / kTile && threadIdx.x == ((n - 1) % kTile) / kIt) out[n] = pre;  // total
 }
 
+#ifndef FM_SCAN_BIG_MIN
+#define FM_SCAN_BIG_MIN (1 << 20)
+#endif
 cudaError_t run_scan_lb(const uint64_t *in, uint64_t *out, int64_t n, void *tmp, size_t tmp_bytes, cudaStream_t st,
                         bool small = false, bool zeroed = false)
 {
-    const int64_t tile = small ? 128 * kItems : kTile;
+    // long arrays: 4096-item tiles (16 per thread) -- the look-back chain is per tile, and a block's
+    // threads wait at its barrier for it (ncu at n = 1e7 with 2048-item tiles: 50 barrier-stall
+    // samples per issued instruction, issue active 11 %)
+    const bool big = !small && n >= FM_SCAN_BIG_MIN;
+    const int64_t tile = small ? 128 * kItems : big ? kThreads * 16 : kTile;
     const int64_t nb = (n + tile - 1) / tile;
     const size_t need = sizeof(uint64_t) * (size_t)(nb + 1);
     if (tmp_bytes < need) return cudaErrorInvalidValue;
@@ -247,11 +254,14 @@ cudaError_t run_scan_lb(const uint64_t *in, uint64_t *out, int64_t n, void *tmp,
     cudaError_t e = zeroed ? cudaSuccess : cudaMemsetAsync(tmp, 0, need, st);
     if (e != cudaSuccess) return e;
     count_launch();
+    uint64_t *status = (uint64_t *)tmp;
+    unsigned int *ticket = (unsigned int *)(status + nb);
     if (small)
-        k_scan_lb<128, 16><<<(unsigned)nb, 128, 0, st>>>(in, out, n, (uint64_t *)tmp, (unsigned int *)((uint64_t *)tmp + nb));
+        k_scan_lb<128, 16, kItems><<<(unsigned)nb, 128, 0, st>>>(in, out, n, status, ticket);
+    else if (big)
+        k_scan_lb<kThreads, 1, 16><<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, status, ticket);
     else
-        k_scan_lb<kThreads, 1><<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, (uint64_t *)tmp,
-                                                                  (unsigned int *)((uint64_t *)tmp + nb));
+        k_scan_lb<kThreads, 1, kItems><<<(unsigned)nb, kThreads, 0, st>>>(in, out, n, status, ticket);
     return cudaGetLastError();
 }
 
