@@ -422,7 +422,11 @@ static fm_status sort_plan_impl(fm_model model, fm_graph kind, int64_t n1, const
     // packed gather records: ECM always (32 B); UBCM one 16-byte (kappa, id) record per candidate at
     // every size (config 2 sampler -3 %, config 5 -4 % against two arrays, once the record's dead
     // word no longer stalled the gather; FM_UBCM_CAND_MIN raises the threshold for A/B runs)
-    const bool want_cand = model == FM_ECM || n2 >= env_i64("FM_UBCM_CAND_MIN", 0);
+    // (not where the sampler takes the rank-out path, N >= FM_UBCM_RANK_OUT_MIN: it gathers kappa
+    // alone there; the statistics mode and overflow re-runs then gather from the two arrays --
+    // config 4: 160 MB and a 44 us pass less per plan)
+    const bool want_cand =
+        model == FM_ECM || (n2 >= env_i64("FM_UBCM_CAND_MIN", 0) && n2 < env_i64("FM_UBCM_RANK_OUT_MIN", int64_t(1) << 21));
     if (want_cand)
         CK(malloc_async_retry((void **)&p->cand, sizeof(double2) * kCandWords(model) * std::max<int64_t>(n2, 1), st),
            "alloc cand");

@@ -87,3 +87,26 @@ def test_config5_degree_gate_without_edge_lists(O):
     z = (m - k) / np.sqrt(kv / R)
     assert np.max(np.abs(z[R * kv >= 25])) < 5.0
     assert abs(int(dp.sum().item()) - 2 * cnt["accepted"]) == 0
+
+
+def test_rank_out_plan_without_records(O, monkeypatch):
+    """A plan above the rank-out threshold holds no (kappa, id) records: the statistics mode and the
+    overflow re-runs gather from the two arrays instead; all agree with the oracle's samples."""
+    monkeypatch.setenv("FM_UBCM_RANK_OUT_MIN", "1000")
+    n = 30_000
+    x, _ = WL.random_fitness(11, n, 2.4, 0.02, ecm=False)
+    plan = fm.sort_plan(torch.from_numpy(x).cuda(), seg_target=64)
+    e = fm.sample_ubcm(plan, 3, n_samples=5, first_sample=2)
+    dp, _, _, _, cnt = fm.sample_degrees(plan, 3, n_samples=5, first_sample=2)
+    assert cnt["accepted"] == e.accepted and cnt["draws"] == e.draws
+    r, _, _, _ = edge_sums(e, n, n, False)
+    assert torch.equal(dp, r)
+    ref = O.sample(O.sort_plan(x, None, seg_target=64), 3, n_samples=5, first_sample=2, nthreads=O.ncores())
+    oe = ref.edges.astype(np.int64)
+    assert np.array_equal(dp.cpu().numpy(), np.bincount(oe[:, 0], minlength=n) + np.bincount(oe[:, 1], minlength=n))
+    assert np.array_equal(np.asarray(e.offsets), ref.offsets)
+    # tiny scratch slots: the overflowed tasks are re-run straight into the list (record-free gathers)
+    monkeypatch.setenv("FM_DEBUG_SCRATCH_CAP", "8")
+    plan2 = fm.sort_plan(torch.from_numpy(x).cuda(), seg_target=64)
+    e2 = fm.sample_ubcm(plan2, 3, n_samples=5, first_sample=2)
+    assert torch.equal(e2.edges, e.edges) and np.array_equal(np.asarray(e2.offsets), np.asarray(e.offsets))
