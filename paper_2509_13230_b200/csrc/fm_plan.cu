@@ -198,7 +198,10 @@ __device__ __forceinline__ int64_t plan_cut(const uint64_t *P, int F, int64_t nc
 
 // a4 step 5-6 (per segment): (u, a, b, sigma), initial bound (x0, d0, h0, omT), work estimate,
 // written straight into the sampler's packed record (SegRec)
-__global__ void __launch_bounds__(256) k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg,
+#ifndef FM_EMIT_MINB
+#define FM_EMIT_MINB 6  // 42 registers: config-4 plan 1.99 -> 1.95 ms (5: 1.96, 8 spills: 2.07)
+#endif
+__global__ void __launch_bounds__(256, FM_EMIT_MINB) k_emit(int model, int kind, int64_t n, int64_t nc, int64_t n_seg,
                                               const double *__restrict__ kappa_s, const double *__restrict__ y_s,
                                               const double *__restrict__ ly_s, const int32_t *__restrict__ perm,
                                               const int32_t *__restrict__ excl, const double *__restrict__ ckappa,
