@@ -219,6 +219,35 @@ int64_t env_i64(const char *name, int64_t dflt)
     return strtoll(v, nullptr, 10);
 }
 
+// Device -> host copy in pieces of FM_D2H_CHUNK_MB (64) MiB: on the B200 boxes one 12.8 GB
+// cudaMemcpyAsync into page-locked memory ran at 51.6 GB/s, the same bytes in 32-256 MiB copies on
+// the same stream at 56 GB/s (scripts/d2h_probe.py); 0: one copy (FM_D2H_CHUNK_KB: tests)
+cudaError_t copy_to_host_chunked(void *dst, const void *src, size_t bytes, cudaStream_t st)
+{
+    const int64_t kb = env_i64("FM_D2H_CHUNK_KB", 0);
+    const int64_t mb = kb > 0 ? 1 : env_i64("FM_D2H_CHUNK_MB", 64);
+    const size_t chunk = kb > 0 ? (size_t)kb << 10 : mb > 0 ? (size_t)mb << 20 : std::max<size_t>(bytes, 1);
+    // a short first piece up to the next 2 MiB boundary of the destination: the pieces of a sample
+    // group that starts in the middle of the list (fm_sample_to_host) ran at 50 GB/s from an
+    // arbitrary byte offset, 56-57 GB/s from an aligned one (FM_PIPE_TRACE timeline of config 5)
+    const size_t al = (size_t)env_i64("FM_D2H_ALIGN", 2 << 20);
+    size_t o = 0;
+    if (mb > 0 && al > 1 && (al & (al - 1)) == 0) {
+        const size_t head = std::min(bytes, (al - ((uintptr_t)dst & (al - 1))) & (al - 1));
+        if (head > 0) {
+            const cudaError_t e = cudaMemcpyAsync(dst, src, head, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return e;
+            o = head;
+        }
+    }
+    for (; o < bytes; o += chunk) {
+        const cudaError_t e = cudaMemcpyAsync((char *)dst + o, (const char *)src + o, std::min(chunk, bytes - o),
+                                              cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 void plan_release(Plan *p)
@@ -1058,12 +1087,11 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                     }
                     if (hi == lo) continue;
                     CK(cudaStreamWaitEvent(copy_st, ev_done[(size_t)g], 0), "copy after compaction");
-                    CK(cudaMemcpyAsync(host->e + 2 * lo, (const int32_t *)own->edges + 2 * lo, sizeof(int32_t) * 2 * (hi - lo),
-                                       cudaMemcpyDeviceToHost, copy_st),
+                    CK(copy_to_host_chunked(host->e + 2 * lo, (const int32_t *)own->edges + 2 * lo, sizeof(int32_t) * 2 * (hi - lo),
+                                            copy_st),
                        "copy edges to the host");
                     if (host->w && own->weights)
-                        CK(cudaMemcpyAsync(host->w + lo, (const int32_t *)own->weights + lo, sizeof(int32_t) * (hi - lo),
-                                           cudaMemcpyDeviceToHost, copy_st),
+                        CK(copy_to_host_chunked(host->w + lo, (const int32_t *)own->weights + lo, sizeof(int32_t) * (hi - lo), copy_st),
                            "copy weights to the host");
                     mark(g, "on host", copy_st);
                 }
@@ -1159,10 +1187,10 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                 host_short = true;  // the device list stays valid: fm_edges_to_host with a larger buffer
             } else if ((!host_done || n_overflow > 0) && total > 0) {
                 // (the list was redone or tasks were re-run into it after the groups' copies)
-                CK(cudaMemcpyAsync(host->e, own->edges, sizeof(int32_t) * 2 * total, cudaMemcpyDeviceToHost, st),
+                CK(copy_to_host_chunked(host->e, own->edges, sizeof(int32_t) * 2 * total, st),
                    "copy edges to the host");
                 if (host->w && own->weights)
-                    CK(cudaMemcpyAsync(host->w, own->weights, sizeof(int32_t) * total, cudaMemcpyDeviceToHost, st),
+                    CK(copy_to_host_chunked(host->w, own->weights, sizeof(int32_t) * total, st),
                        "copy weights to the host");
                 CK(cudaStreamSynchronize(st), "sync (copy to the host)");
             }
@@ -1359,10 +1387,10 @@ fm_status fm_edges_to_host(const fm_edges *e, int32_t *edges_host, int32_t *weig
     cudaStream_t st = (cudaStream_t)cuda_stream;
     if (e->n_edges > 0) {
         if (!edges_host) return fail(FM_ERR_INVALID, "edges_host is NULL");
-        CK(cudaMemcpyAsync(edges_host, e->edges, sizeof(int32_t) * 2 * e->n_edges, cudaMemcpyDeviceToHost, st),
+        CK(copy_to_host_chunked(edges_host, e->edges, sizeof(int32_t) * 2 * e->n_edges, st),
            "copy edges");
         if (weights_host && e->weights)
-            CK(cudaMemcpyAsync(weights_host, e->weights, sizeof(int32_t) * e->n_edges, cudaMemcpyDeviceToHost, st),
+            CK(copy_to_host_chunked(weights_host, e->weights, sizeof(int32_t) * e->n_edges, st),
                "copy weights");
     }
     CK(cudaStreamSynchronize(st), "sync (to_host)");

@@ -298,7 +298,9 @@ def test_no_device_memory_leak():
 
 
 @pytest.mark.parametrize("ecm", [False, True])
-@pytest.mark.parametrize("env", [{}, {"FM_HOST_GROUPS": "3"}, {"FM_DEBUG_SCRATCH_CAP": "8"}, {"FM_HOST_GROUPS": "1"}])
+@pytest.mark.parametrize("env", [{}, {"FM_HOST_GROUPS": "3"}, {"FM_DEBUG_SCRATCH_CAP": "8"}, {"FM_HOST_GROUPS": "1"},
+                                 {"FM_HOST_GROUPS": "3", "FM_D2H_CHUNK_KB": "4", "FM_D2H_ALIGN": "256"},  # many aligned pieces
+                                 {"FM_D2H_CHUNK_MB": "0"}])
 def test_sample_to_host(O, monkeypatch, ecm, env):
     """fm_sample_to_host: the host buffers hold the oracle's list (copied group by group while later
     groups are sampled), also after forced slot overflows (re-run tasks: copied again); too small
