@@ -1132,6 +1132,8 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
                 CK(cudaStreamSynchronize(st), "sync (sample)");
             }
             if (ptrace && t_0) {
+                if (host)
+                    fprintf(stderr, "[pipe] device list %p, host buffer %p\n", (const void *)own->edges, (const void *)host->e);
                 for (const Mark &m : marks) {
                     float ms = 0.f;
                     cudaEventElapsedTime(&ms, t_0, m.e);

@@ -1,6 +1,6 @@
 """profiles/<tag>_summary.md for a round-2 evidence run (scripts/gpu/r02_final.sh), from the files it left:
 
-    python scripts/make_summary_r02.py r02_v11
+    python scripts/make_summary_r02.py r02_v12
 
 reads profiles/<tag>_bench_{default,cfg2,cfg3,cfg4,reference}.json, <tag>_cfg{5,2,3,4}_ncu_raw.csv (raw-page
 exports of the ncu --set full captures), <tag>_launches_cfg{5,4}.csv and <tag>_pytest.log.
@@ -86,6 +86,11 @@ if r:
     cb = r["cpu_baseline"]
     out += ["", f"Reference arm (`--impl reference`: the CPU oracle on {cb['cores']} host cores, {cb['sample']}): "
             f"{r['value']:.3e} {r['unit']}."]
+b2 = bench("default_box2")
+if b2:
+    out += ["", f"The e2e leg is PCIe-bound and varies with the box: the default line re-run on a second box (`{tag}_bench_default_box2.json`): "
+            f"{b2['value']:.3e} edges/s, e2e {b2['e2e']['value']:.3e} edges/s, {b2['e2e']['ms_per_step']:.1f} ms per step "
+            f"({b2['e2e']['d2h_gbs']:.1f} GB/s; first box: {d['e2e']['d2h_gbs']:.1f} GB/s)."]
 if d:
     rf = d["roofline"]
     out += ["", f"Default line's roofline object: bound `{rf['bound']}`, achieved {rf['achieved']:.4g} of peak {rf['peak']:.4g} {rf['unit']} "
