@@ -187,7 +187,8 @@ fm_status fm_expected_degrees(fm_model model, int64_t n, const double *x, const 
  * groups of samples and copies each group's part of the list to the host while the next groups are
  * still being sampled, so the device -> host transfer (the bound of the host path: 8 B per edge over
  * PCIe) starts after the first group instead of after the whole call.  Use page-locked host memory
- * for the copies to be asynchronous.  `out` is filled as by fm_sample_* (the device list stays
+ * for the copies to be asynchronous (both host copies go in 64 MiB pieces that start at 2 MiB
+ * boundaries of the destination: the rate of the transfer depends on that alignment).  `out` is filled as by fm_sample_* (the device list stays
  * valid until fm_free).  If the list holds more than host_cap edges, out->flags has
  * FM_FLAG_HOST_TRUNCATED, the host buffers hold nothing valid, and fm_edges_to_host can be called
  * with larger buffers.  Same results as fm_sample_*; synchronises the stream. */
