@@ -750,13 +750,15 @@ static fm_status sample_impl(int model, const fm_plan *plan_, uint64_t seed, int
     // fastest on all five configs; the option stays for callers short of memory (scratch is 2/G).
     int64_t G = 1;
     if (n_samples > 1 && small_compact && !fuse) {
-        // (a host destination: one group per ~2 GB of expected list, at most 8 -- the call is bound
-        // by the D2H copies (8 B per edge over PCIe, ~55 GB/s), which hide the groups' tails; below
-        // ~4 GB the overlap gains less than the groups cost: measured -10 % on configs 3 and 4)
+        // (a host destination: one group per ~0.8 GB of expected list, 4 to 16 of them from 256 MB --
+        // the call is bound by the D2H copies (8 B per edge over PCIe, ~55 GB/s), which hide the
+        // groups' tails; with the copies in aligned pieces: config 5 236 -> 233 ms with 16 groups
+        // instead of 6 (32: 232), configs 2-4 -2 % with 4 groups instead of 1 (2 groups: +-0))
         int64_t hg = 1;
         if (host && host->e) {
             const double bytes = 8.0 * (double)std::max<int64_t>(1, p->est_draws - p->n_seg) * (double)n_samples;
-            hg = env_i64("FM_HOST_GROUPS", std::min<int64_t>(8, (int64_t)(bytes / 2e9)));
+            const int64_t auto_g = bytes < 256e6 ? 1 : std::min<int64_t>(16, std::max<int64_t>(4, (int64_t)(bytes / 0.8e9)));
+            hg = env_i64("FM_HOST_GROUPS", auto_g);
         }
         const int64_t forced = env_i64("FM_SAMPLE_GROUPS", std::max<int64_t>(1, hg));
         if (forced > 0) G = forced;
