@@ -1,6 +1,6 @@
 # round-2 final evidence: r02_profile.sh (tests, smoke, bench lines, config-5 launch list, ncu full of configs 5 and 2)
 # + the ECM capture, the config-4 launch list and the config-4 sampler / compaction capture
-TAG=${TAG:-r02_v12}
+TAG=${TAG:-r02_v13}
 export TAG
 bash scripts/gpu/r02_profile.sh
 ncu --set full --clock-control none --import-source on -k regex:"k_sample|k_compact" -s 2 -c 2 -f -o gpurun_out/${TAG}_cfg3_prof python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_3.log 2>&1

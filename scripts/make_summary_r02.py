@@ -1,6 +1,6 @@
 """profiles/<tag>_summary.md for a round-2 evidence run (scripts/gpu/r02_final.sh), from the files it left:
 
-    python scripts/make_summary_r02.py r02_v12
+    python scripts/make_summary_r02.py r02_v13
 
 reads profiles/<tag>_bench_{default,cfg2,cfg3,cfg4,reference}.json, <tag>_cfg{5,2,3,4}_ncu_raw.csv (raw-page
 exports of the ncu --set full captures), <tag>_launches_cfg{5,4}.csv and <tag>_pytest.log.
